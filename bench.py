@@ -1,0 +1,379 @@
+"""SC-decode throughput bench (BASELINE.json metric: SC-decoded Mbit/s).
+
+python bench.py [--gpus N] [--steps K] [--warmup W] [--config c3] [--impl ours|reference]
+
+A step = one batched decode of this rank's frames of the config (c3 by
+default: BSC p=0.02, N=2^20, rate 0.83, 256 frames per GPU, the reference's
+own frozen set).  Mbit/s = frames * N / seconds / 1e6 (block bits).
+
+  value    device-resident fp32 LLRs (+ revealed frozen words) in HBM, u-hat
+           written to HBM, CUDA events on the launching stream, L2 flushed
+           (256 MiB write) between timed steps, max over ranks.
+  e2e      the public API with host buffers: each step copies Bob's inputs from
+           pinned host memory (BSC: received bits packed 1 bit/symbol, decoded
+           by the fused front end; BIAWGN: fp32 LLRs) plus the revealed frozen
+           words, decodes, and copies u-hat back.
+Multi-GPU (torchrun): frames shard by index (rank r takes frames
+[r*F, (r+1)*F)), no collective on the hot path; NCCL all-reduces the frame
+error counts afterwards (scaling: weak).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+from concurrent.futures import ThreadPoolExecutor
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+PAPER_MBPS = {"c3": 9.5}  # BASELINE.md / PAPER.md:170: SC decode, BSC 2%, N=2^20, 1 core i5-670
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="c3")
+    ap.add_argument("--frames", type=int, default=0, help="frames per GPU (default: the config's)")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--fmode", default="exact", choices=["exact", "min-sum"])
+    ap.add_argument("--no-ssc", action="store_true")
+    ap.add_argument("--cpu-sample-s", type=float, default=10.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+def dist_env():
+    return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
+
+
+def gen_frames(cfg, N, j0, F):
+    """Bob's inputs for frames j0..j0+F-1 (seed convention of channel.frame)."""
+    from paper_1204_5882_b200 import channel as C
+
+    x = np.empty((F, N), np.uint8)
+    llr = np.empty((F, N), np.float32)
+    y_bits = np.empty((F, N), np.uint8) if isinstance(cfg.channel, C.Bsc) else None
+
+    def one(i):
+        xi, yi = C.frame(cfg.channel, cfg.seed, j0 + i, N)
+        x[i] = xi
+        llr[i] = C.channel_llr(cfg.channel, yi)
+        if y_bits is not None:
+            y_bits[i] = yi
+
+    with ThreadPoolExecutor(max_workers=min(16, os.cpu_count() or 4)) as ex:
+        list(ex.map(one, range(F)))
+    return x, llr, y_bits
+
+
+class ClockSampler:
+    """nvidia-smi's clocks line, via NVML, sampled during the timed region."""
+
+    REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+               0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
+               0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+               0x100: "display_clock_setting"}
+
+    def __init__(self, index):
+        self.ok = False
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception as e:  # pragma: no cover
+            self.err = str(e)
+        self.samples, self.reasons = [], 0
+        self._stop = threading.Event()
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                self.reasons |= self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+            except Exception:
+                pass
+            time.sleep(0.05)
+
+    def __enter__(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self.ok:
+            self.t.join()
+
+    def summary(self):
+        if not self.ok or not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
+        rs = [name for bit, name in self.REASONS.items() if self.reasons & bit and bit != 0x1]
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max, "reasons": rs,
+                "samples": len(self.samples)}
+
+
+def cpu_baseline(code, llr, u, sample_s, threads=1):
+    """The oracle port (f64 exact SC, SPEC restatement) on host cores: decode
+    frames until ~sample_s of CPU work; Mbit/s of block bits."""
+    from oracle import oracle as O
+
+    N = code.block_size
+    F = llr.shape[0]
+    done, t0 = 0, time.perf_counter()
+    while True:
+        k = min(threads, F - (done % F))
+        idx = [(done + i) % F for i in range(k)]
+        O.sc_decode_batch(code.frozen_mask, llr[idx], u[idx], precision=64, threads=threads)
+        done += k
+        el = time.perf_counter() - t0
+        if el >= sample_s or done >= 4 * F:
+            break
+    return done * N / el / 1e6, done, el
+
+
+def roofline_entry(code, frames, log2S, t_kernel_s, peaks):
+    """Dominant kernel: sc_decode_kernel.  Algorithmic bytes per launch =
+    SURVEY.md 8(d)'s 12.3125 N bytes per HBM-streamed level per frame x the
+    levels this launch streams through the per-frame scratch (n - log2 S)."""
+    n = code.n
+    L_up = max(0, n - log2S)
+    alg = 12.3125 * code.block_size * frames * L_up
+    peak = peaks.get("hbm_gbs", 6650.0)
+    achieved = alg / t_kernel_s / 1e9 if t_kernel_s > 0 else 0.0
+    return {"bound": "hbm", "achieved": round(achieved, 2), "peak": peak, "unit": "GB/s",
+            "frac": round(achieved / peak, 4), "traffic": None,
+            "kernel": "sc_decode_kernel", "alg_bytes_per_launch": alg, "upper_levels": L_up,
+            "peak_source": "MEASURED_PEAKS.json" if "hbm_gbs" in peaks else "fallback B200_PROFILING.md"}
+
+
+def run_reference(args, rank, world):
+    """--impl reference: the reference's decode path has no implementation
+    (polar_core is SPEC-only), so the CPU oracle port -- the SPEC restatement --
+    is timed on all host threads, one frame per thread per step."""
+    if rank != 0:
+        return
+    from oracle import oracle as O
+    from paper_1204_5882_b200 import codes as K
+
+    cfg = K.CONFIGS[args.config]
+    code = K.load_config(args.config)
+    N = code.block_size
+    threads = max(1, len(os.sched_getaffinity(0)))
+    F = threads
+    x, llr, _ = gen_frames(cfg, N, 0, F)
+    u = np.array([O.polar_transform_bytes(xi) for xi in x])
+    times = []
+    for s in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        O.sc_decode_batch(code.frozen_mask, llr, u, precision=64, threads=threads)
+        dt = time.perf_counter() - t0
+        if s >= args.warmup:
+            times.append(dt)
+    tot = sum(times)
+    v = F * N * len(times) / tot / 1e6
+    line = {"metric": "SC-decoded Mbit/s", "value": round(v, 3), "unit": "Mbit/s", "n_gpus": 0,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(1e3 * tot / len(times), 3),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (reference channel model, seeded)", "impl": "reference",
+            "config": {"workload": cfg.desc, "key": args.config, "frames_per_step": F, "N": N},
+            "cpu_baseline": {"value": round(v, 3), "unit": "Mbit/s", "cores": threads, "kind": "port",
+                             "sample": f"{F} frames of {args.config} per step (one per thread), f64 exact SC"},
+            "e2e": {"value": round(v, 3), "unit": "Mbit/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    rank, world, local = dist_env()
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_1204_5882_b200 import codes as K
+    from paper_1204_5882_b200.channel import Bsc
+    from paper_1204_5882_b200.polar_core import ScDecoder, pack_bits, polar_transform_words
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    cfg = K.CONFIGS[args.config]
+    code = K.load_config(args.config)
+    N, n = code.block_size, code.n
+    F = args.frames or cfg.frames_per_gpu
+    is_bsc = isinstance(cfg.channel, Bsc)
+
+    x, llr, y_bits = gen_frames(cfg, N, rank * F, F)
+    x_w = torch.from_numpy(pack_bits(x).view(np.int32).copy()).to(dev)
+    u_w = polar_transform_words(x_w, n)  # Alice: u = T(x); the decoder reads u at frozen positions
+    llr_d = torch.from_numpy(llr).to(dev)
+    dec = ScDecoder(code, max_frames=F, f_mode=args.fmode, ssc=not args.no_ssc)
+    uh = dec.alloc_words(F)
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.int32, device=dev)  # 256 MiB > L2
+    stream = torch.cuda.current_stream()
+
+    def step():
+        dec.decode(llr_d, u_w, u_hat=uh, stream=stream)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    errors = int((uh != u_w).any(dim=1).sum().item())
+    launches = dec.last_launches
+    log2S = dec_log2S(dec, F)
+
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    sampler = ClockSampler(local)
+    t_wall = time.perf_counter()
+    with sampler:
+        for i in range(args.steps):
+            flush.fill_(i)
+            ev[i][0].record(stream)
+            step()
+            ev[i][1].record(stream)
+        torch.cuda.synchronize()
+    t_wall = time.perf_counter() - t_wall
+    if world > 1:
+        dist.barrier()
+    t_dev = sum(a.elapsed_time(b) for a, b in ev) / 1e3
+    t_max = torch.tensor([t_dev], device=dev)
+    if world > 1:
+        dist.all_reduce(t_max, op=dist.ReduceOp.MAX)
+    t_max = float(t_max.item())
+    ms_step = 1e3 * t_max / args.steps
+    value = world * F * N * args.steps / t_max / 1e6
+
+    # kernel-only time of the dominant kernel on the same stream
+    kt = []
+    for i in range(min(args.steps, 5)):
+        flush.fill_(i)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        dec.decode(llr_d, None, u_hat=None, want_u=False, stream=stream)
+        b.record(stream)
+        kt.append((a, b))
+    torch.cuda.synchronize()
+    t_kernel = statistics.median(a.elapsed_time(b) for a, b in kt) / 1e3
+
+    # ---- end to end through the public API with host buffers
+    e2e = None
+    if not args.no_e2e:
+        if is_bsc:
+            h_in = torch.from_numpy(pack_bits(y_bits).view(np.int32).copy()).pin_memory()
+            d_in = torch.empty_like(h_in, device=dev)
+        else:
+            h_in = torch.from_numpy(llr).pin_memory()
+            d_in = torch.empty_like(h_in, device=dev)
+        h_fz = u_w.cpu().pin_memory()
+        d_fz = torch.empty_like(u_w)
+        h_out = torch.empty((F, dec.wpf), dtype=torch.int32).pin_memory()
+        mag = cfg.channel.llr_magnitude if is_bsc else 0.0
+
+        def e2e_step():
+            d_in.copy_(h_in, non_blocking=True)
+            d_fz.copy_(h_fz, non_blocking=True)
+            if is_bsc:
+                dec.decode_bsc(d_in, mag, d_fz, u_hat=uh, stream=stream)
+            else:
+                dec.decode(d_in, d_fz, u_hat=uh, stream=stream)
+            h_out.copy_(uh, non_blocking=True)
+
+        for _ in range(2):
+            e2e_step()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for _ in range(args.steps):
+            e2e_step()
+        b.record(stream)
+        torch.cuda.synchronize()
+        te = torch.tensor([a.elapsed_time(b) / 1e3], device=dev)
+        if world > 1:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        te = float(te.item())
+        hb = h_in.numel() * h_in.element_size() + h_fz.numel() * 4
+        e2e = {"value": round(world * F * N * args.steps / te / 1e6, 2), "unit": "Mbit/s",
+               "h2d_bytes_per_step": int(hb), "d2h_bytes_per_step": int(h_out.numel() * 4),
+               "input": "received bits, fused BSC front end" if is_bsc else "fp32 LLRs"}
+        err2 = int((uh != u_w).any(dim=1).sum().item())
+        assert err2 == errors, "e2e path decoded differently from the device path"
+
+    # statistics off the hot path (NCCL all-reduce of frame errors)
+    stats = torch.tensor([errors, F], dtype=torch.int64, device=dev)
+    if world > 1:
+        dist.all_reduce(stats)
+
+    if rank == 0:
+        peaks = {}
+        try:
+            with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+                peaks = json.load(fh)
+        except Exception:
+            pass
+        cpu = None
+        if not args.no_cpu_baseline:
+            from oracle import oracle as O
+            u_np = np.array([O.polar_transform_bytes(xi) for xi in x[:8]])
+            v, nfr, el = cpu_baseline(code, llr[:8], u_np, args.cpu_sample_s, threads=1)
+            cpu = {"value": round(v, 3), "unit": "Mbit/s", "cores": 1, "kind": "port",
+                   "sample": f"{nfr} frames of {args.config} (N=2^{n}) in {el:.1f} s, f64 exact SC, 1 thread"}
+        line = {
+            "metric": "SC-decoded Mbit/s", "value": round(value, 2), "unit": "Mbit/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 3),
+            "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": round(value / PAPER_MBPS[args.config], 1) if args.config in PAPER_MBPS else None,
+            "dtype": "f32" if args.fmode == "exact" else "f32-minsum",
+            "data": "synthetic: reference channel model, seeded (SURVEY 8(d)); reference-constructed frozen set",
+            "config": {"workload": cfg.desc, "key": args.config, "frames_per_gpu": F, "N": N,
+                       "rate": cfg.rate, "f": args.fmode, "ssc": not args.no_ssc, "subtree_log2": log2S,
+                       "parallelism": f"frames sharded over {world} GPU(s)", "l2": "256 MiB flush between steps"},
+            "fer": round(int(stats[0]) / int(stats[1]), 4), "frames_total": int(stats[1]),
+            "e2e": e2e, "gpu_launches": launches * args.steps,
+            "roofline": roofline_entry(code, F, log2S, t_kernel, peaks),
+            "kernel_ms": round(1e3 * t_kernel, 3),
+            "cpu_baseline": cpu, "clocks": sampler.summary(), "wall_s_timed": round(t_wall, 3),
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def dec_log2S(dec, F):
+    """Mirror of the library's automatic sub-tree size choice (for reporting)."""
+    import torch
+    sm = torch.cuda.get_device_properties(dec.device).multi_processor_count
+    per_sm = -(-F // sm)
+    best = 6
+    for k in range(6, 15):
+        S = 1 << k
+        if per_sm * (8 * S + (S // 32) * 4 + 2 * S) <= 200 * 1024:
+            best = k
+    return min(best, dec.n)
+
+
+if __name__ == "__main__":
+    main()

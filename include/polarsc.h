@@ -1,0 +1,119 @@
+/*
+ * polarsc.h -- C ABI of the B200-native polar-code SC decoder.
+ *
+ * Plain pointers and sizes only; no torch types.  Every device pointer is
+ * caller-owned CUDA device memory; every call is stream-ordered and
+ * asynchronous (no implicit device synchronisation).  A handle owns its
+ * device scratch (allocated once in pq_decoder_create, never inside decode)
+ * and is not thread-safe: use one handle per host thread / stream
+ * ("a decoder instance owns its scratch buffers and is
+ * single-threaded; instances are independent").
+ *
+ * Bit vectors (u-domain and x-domain BitBlocks) are packed
+ * uint32 words, bit i of a frame at word i>>5, bit position i&31 (LSB first),
+ * the same order as the reference's code-table mask packing
+ * (np.packbits(..., bitorder="little"), construction.py:644 / :668).
+ * Frames are stored frame-major: frame f's words start at f * (N/32)
+ * (N >= 32; for N < 32 each frame still occupies one word).
+ *
+ * Return codes: 0 = ok; negative = invalid argument (Python: ValueError);
+ * positive = CUDA/runtime failure (Python: RuntimeError).  pq_last_error()
+ * returns the text of the most recent failure on the calling thread.
+ *
+ * Reference interfaces replaced (the reference's polar_core is specified in
+ * /root/reference/SPEC.md but not implemented; its construction->decoding
+ * contract is PolarCode in pkg/src/polarqkd/construction.py):
+ */
+#ifndef POLARSC_H
+#define POLARSC_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PQ_ABI_VERSION 1
+
+/* f-function modes.  EXACT is the SPEC's phi-form boxplus (SPEC.md:243,
+ * SPEC.md:270 "exact phi-based form, not min-sum"); MINSUM is the opt-in
+ * approximation named by the north star (no reference counterpart).        */
+#define PQ_F_EXACT 0
+#define PQ_F_MINSUM 1
+
+/* options for pq_decoder_set_option */
+#define PQ_OPT_SSC 1          /* 1 (default): skip rate-0/rate-1/repetition sub-trees
+                                 (decision-exact); 0: plain SC          */
+#define PQ_OPT_SUBTREE_LOG2 2 /* log2 of the shared-memory sub-tree width S; 0 = auto  */
+#define PQ_OPT_FMODE 3        /* PQ_F_EXACT / PQ_F_MINSUM                              */
+
+typedef struct pq_decoder pq_decoder;
+
+/* Create a decoder for block length N = 2^n (1 <= n <= 25) and up to
+ * max_frames frames per call on CUDA device `device`.
+ * Replaces: constructing a polar_core decoder instance.  */
+int pq_decoder_create(pq_decoder **out, int n, int max_frames, int f_mode, int device);
+
+/* Install the frozen set: mask_host[i] = 1 if position i is frozen, length
+ * 2^n bytes -- exactly PolarCode.frozen_mask (construction.py:264-268).
+ * The mask is copied; the handle is immutable w.r.t. the code afterwards. */
+int pq_decoder_set_frozen_mask(pq_decoder *h, const uint8_t *mask_host);
+
+int pq_decoder_set_option(pq_decoder *h, int key, int value);
+int pq_decoder_get_option(const pq_decoder *h, int key);
+
+/* Batched float SC decode.
+ * Replaces: sc_decode(code, llrs, frozen_values) -> u_hat,
+ *           applied to `frames` independent blocks.
+ *   llr       [frames][N] fp32 channel LLRs (positive favours 0, channel.py:14)
+ *   frozen_u  [frames][N/32] packed u-domain words whose bits at frozen
+ *             positions are the revealed frozen values;
+ *             bits at information positions are ignored.  NULL = all zero.
+ *   u_hat     [frames][N/32] out: decoded u (frozen positions carry exactly
+ *             the revealed values).  May be NULL.
+ *   x_hat     [frames][N/32] out: x_hat = polar_transform(u_hat) (what
+ *             bob_decode re-encodes).  May be NULL.
+ *   stream    cudaStream_t (NULL = legacy default stream).                 */
+int pq_sc_decode_f32(pq_decoder *h, const float *llr, const uint32_t *frozen_u,
+                     uint32_t *u_hat, uint32_t *x_hat, int frames, void *stream);
+
+/* Same, plain SC (no sub-tree shortcuts) with every stage LLR written to
+ * dump [frames][n+1][N]: dump[f][d][j*W + t] = element t of node j at depth
+ * d, W = N >> d (the canonical stage dump of SURVEY.md App. A.6), in the
+ * coset-shifted domain (each node's LLRs are sign-flipped by
+ * the node-level codeword of the frozen values).  Parity/debug only.     */
+int pq_sc_decode_f32_dump(pq_decoder *h, const float *llr, const uint32_t *frozen_u,
+                          uint32_t *u_hat, uint32_t *x_hat, float *dump, int frames,
+                          void *stream);
+
+/* BSC front end fused into the decoder's level-0 reads: y_bits are Bob's
+ * received bits packed like u_hat; the channel LLR (1-2y)*llr_mag is formed
+ * on the fly (channel.py:142-147 with magnitude min(30, ln((1-p)/p))).
+ * Replaces: channel_llr(Bsc(p), obs) followed by sc_decode (bob_decode's
+ * first two steps).                                          */
+int pq_sc_decode_bsc(pq_decoder *h, const uint32_t *y_bits, float llr_mag,
+                     const uint32_t *frozen_u, uint32_t *u_hat, uint32_t *x_hat, int frames,
+                     void *stream);
+
+/* x = u F^{(x)n} over GF(2), natural order, involution, on packed frames.
+ * in and out may alias.  Replaces: polar_transform(u),
+ * also alice_disclose's u = polar_transform(x).             */
+int pq_polar_transform(const uint32_t *in, uint32_t *out, int n, int frames, void *stream);
+
+/* Bytes of device scratch owned by the handle. */
+size_t pq_decoder_workspace_bytes(const pq_decoder *h);
+
+/* Number of kernels the last decode call launched (for bench accounting). */
+int pq_decoder_last_launches(const pq_decoder *h);
+
+int pq_decoder_destroy(pq_decoder *h);
+
+const char *pq_last_error(void);
+int pq_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* POLARSC_H */

@@ -1,0 +1,76 @@
+"""ctypes binding to the in-tree C-ABI library (include/polarsc.h).
+
+There is deliberately no fallback: if libpolarsc.so is missing or no CUDA
+device is present, every decode/transform call raises.  The CPU oracle under
+oracle/ is test infrastructure and is never reachable from here.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libpolarsc.so")
+
+PQ_F_EXACT = 0
+PQ_F_MINSUM = 1
+PQ_OPT_SSC = 1
+PQ_OPT_SUBTREE_LOG2 = 2
+PQ_OPT_FMODE = 3
+
+# every symbol include/polarsc.h declares (tests check the .so exports them)
+EXPORTS = (
+    "pq_decoder_create", "pq_decoder_set_frozen_mask", "pq_decoder_set_option",
+    "pq_decoder_get_option", "pq_sc_decode_f32", "pq_sc_decode_f32_dump", "pq_sc_decode_bsc",
+    "pq_polar_transform", "pq_decoder_workspace_bytes", "pq_decoder_last_launches",
+    "pq_decoder_destroy", "pq_last_error", "pq_abi_version",
+)
+
+_lib = None
+
+
+class PolarScError(RuntimeError):
+    pass
+
+
+def load():
+    """Load libpolarsc.so (raises if it is absent -- build() first)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise PolarScError(
+            f"{LIB_PATH} is missing: run `python -c 'import __graft_entry__ as g; g.build()'` "
+            "(there is no CPU fallback)")
+    L = ctypes.CDLL(LIB_PATH)
+    vp, i, u32p = ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p
+    L.pq_decoder_create.argtypes = [ctypes.POINTER(vp), i, i, i, i]
+    L.pq_decoder_set_frozen_mask.argtypes = [vp, ctypes.c_char_p]
+    L.pq_decoder_set_option.argtypes = [vp, i, i]
+    L.pq_decoder_get_option.argtypes = [vp, i]
+    L.pq_sc_decode_f32.argtypes = [vp, vp, u32p, u32p, u32p, i, vp]
+    L.pq_sc_decode_f32_dump.argtypes = [vp, vp, u32p, u32p, u32p, vp, i, vp]
+    L.pq_sc_decode_bsc.argtypes = [vp, u32p, ctypes.c_float, u32p, u32p, u32p, i, vp]
+    L.pq_polar_transform.argtypes = [u32p, u32p, i, i, vp]
+    L.pq_decoder_workspace_bytes.argtypes = [vp]
+    L.pq_decoder_workspace_bytes.restype = ctypes.c_size_t
+    L.pq_decoder_last_launches.argtypes = [vp]
+    L.pq_decoder_destroy.argtypes = [vp]
+    L.pq_last_error.restype = ctypes.c_char_p
+    L.pq_abi_version.restype = ctypes.c_int
+    for name in EXPORTS:
+        getattr(L, name)
+    _lib = L
+    return L
+
+
+def check(rc: int, what: str) -> None:
+    """Map C-ABI return codes onto the reference's error behaviour:
+    negative -> ValueError (bad arguments, as the reference raises), positive
+    -> PolarScError (CUDA failure)."""
+    if rc == 0:
+        return
+    msg = load().pq_last_error().decode(errors="replace")
+    if rc < 0:
+        raise ValueError(f"{what}: {msg}")
+    raise PolarScError(f"{what}: {msg} (rc={rc})")

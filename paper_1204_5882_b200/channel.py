@@ -1,0 +1,120 @@
+"""Channel models and seeded inputs -- the decoder's input contract.
+
+Restates the parts of the reference's ``polarqkd.channel`` that produce the
+decoder's inputs, with identical semantics so that identical seeds give
+identical frames on a box where the reference is not installed
+(tests/test_channel.py pins every function against the reference's own
+outputs, committed as golden fixtures).
+
+* LLR convention: natural log, positive favours bit 0; channel LLRs are
+  clamped at +-LLR_CLAMP                      (channel.py:10-18, :29)
+* ``make_rng``: PCG64 seeded through SeedSequence((seed, stream))
+                                              (channel.py:66-73)
+* ``transmit``: BSC flips with probability p; BIAWGN sends 1-2b plus
+  N(0, 1/snr)                                 (channel.py:116-133)
+* ``channel_llr``: BSC (1-2y) min(30, ln((1-p)/p)); BIAWGN clip(2 y snr, +-30)
+                                              (channel.py:136-150)
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+from typing import Union
+
+import numpy as np
+
+LLR_CLAMP = 30.0
+
+
+@dataclass(frozen=True)
+class Bsc:
+    """Binary symmetric channel, crossover probability p (channel.py:32-44)."""
+
+    p: float
+
+    def __post_init__(self):
+        if not 0.0 <= self.p <= 0.5:
+            raise ValueError(f"BSC crossover probability must be in [0, 0.5], got {self.p}")
+
+    @property
+    def llr_magnitude(self) -> float:
+        if self.p == 0.0:
+            return LLR_CLAMP
+        if self.p >= 0.5:
+            return 0.0
+        return min(LLR_CLAMP, float(np.log((1.0 - self.p) / self.p)))
+
+
+@dataclass(frozen=True)
+class BiAwgn:
+    """Binary-input AWGN channel, snr = Es / sigma^2 (channel.py:47-60)."""
+
+    snr: float
+
+    def __post_init__(self):
+        if not self.snr > 0.0:
+            raise ValueError(f"BIAWGN snr must be positive, got {self.snr}")
+
+    @property
+    def sigma2(self) -> float:
+        return 1.0 / self.snr
+
+
+ChannelModel = Union[Bsc, BiAwgn]
+
+
+def make_rng(seed, stream=None) -> np.random.Generator:
+    entropy = seed if stream is None else (seed, stream)
+    return np.random.Generator(np.random.PCG64(np.random.SeedSequence(entropy)))
+
+
+def transmit(ch: ChannelModel, bits, seed, stream=None) -> np.ndarray:
+    bits = np.asarray(bits)
+    if bits.size == 0:
+        raise ValueError("transmit requires a nonempty bit vector")
+    rng = make_rng(seed, stream)
+    if isinstance(ch, Bsc):
+        flip = (rng.random(bits.size) < ch.p).astype(np.uint8)
+        return bits.astype(np.uint8) ^ flip
+    if isinstance(ch, BiAwgn):
+        return (1.0 - 2.0 * bits.astype(np.float64)) + rng.normal(0.0, np.sqrt(ch.sigma2), bits.size)
+    raise TypeError(f"unsupported channel model: {ch!r}")
+
+
+def channel_llr(ch: ChannelModel, obs) -> np.ndarray:
+    obs = np.atleast_1d(np.asarray(obs))
+    if isinstance(ch, Bsc):
+        return (1.0 - 2.0 * obs.astype(np.float64)) * ch.llr_magnitude
+    if isinstance(ch, BiAwgn):
+        return np.clip(2.0 * obs.astype(np.float64) * ch.snr, -LLR_CLAMP, LLR_CLAMP)
+    raise TypeError(f"unsupported channel model: {ch!r}")
+
+
+def channel_tag(ch: ChannelModel) -> tuple[int, float]:
+    if isinstance(ch, Bsc):
+        return 0, ch.p
+    if isinstance(ch, BiAwgn):
+        return 1, ch.snr
+    raise TypeError(f"unsupported channel model: {ch!r}")
+
+
+def channel_from_tag(tag: int, param: float) -> ChannelModel:
+    if tag == 0:
+        return Bsc(param)
+    if tag == 1:
+        return BiAwgn(param)
+    raise ValueError(f"unknown channel tag {tag}")
+
+
+# --------------------------------------------------------------------------
+# frame generation (the builder's seed convention, SURVEY.md 8(d) "Seeds"):
+# frame j's key bits come from make_rng(seed, 2j), its channel noise from
+# transmit(ch, x, seed, stream=2j+1); frames are independent of GPU count.
+
+def frame_bits(seed: int, j: int, N: int) -> np.ndarray:
+    return make_rng(seed, 2 * j).integers(0, 2, N, dtype=np.uint8)
+
+
+def frame(ch: ChannelModel, seed: int, j: int, N: int):
+    """(x bits uint8[N], observation y) for frame j."""
+    x = frame_bits(seed, j, N)
+    return x, transmit(ch, x, seed, stream=2 * j + 1)

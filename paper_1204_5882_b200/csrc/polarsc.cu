@@ -1,0 +1,975 @@
+// polarsc.cu -- B200-native (sm_100a) successive-cancellation decoder for
+// polar codes, behind the C ABI declared in include/polarsc.h.
+//
+// What is computed is SPEC.md's sc_decode: Arikan's SC
+// recursion with the exact boxplus f, g(a,b,s) =
+// b + (1-2s)a, decisions in index order, frozen leaves taking the revealed
+// values, natural-order F^{(x)n}.  How it is computed is
+// B200-first; see DESIGN.md for the full argument.  In short:
+//
+//  * Coset shift.  Bob knows the revealed frozen u-values v.  With
+//    c = polar_transform(v restricted to the frozen set) every node's LLR
+//    vector is the textbook one with signs flipped by the node-level codeword
+//    of c.  IEEE negation/addition are sign-symmetric and |f| depends only on
+//    magnitudes, and the tie rule [L < 0] ignores the sign of zero, so
+//    decoding the sign-flipped channel LLRs with all-zero frozen bits makes
+//    exactly the same decisions.  The decoder core therefore never needs
+//    per-frame frozen values: rate-0 sub-trees have all-zero partial sums.
+//  * One CTA per frame walks the whole tree (no host round trips, no
+//    per-level launches).  Levels wider than S live in a per-frame HBM/L2
+//    scratch; the S-wide sub-tree below is staged in shared memory; sub-trees
+//    of width <= 64 are decoded by one warp with LLRs in registers and
+//    shuffles (the north star's "bottom five stages by warp shuffles").
+//  * Partial sums are bit-packed and kept in place: after node (d,j) is done
+//    the bits [jW,(j+1)W) hold T_W(u-hat of that node); a right child's exit
+//    XORs into its left sibling, so the frame's final bit array is x-hat
+//    (shifted) and u-hat = T(x-hat) comes from the XOR-butterfly kernel.
+//  * Decision-exact sub-tree shortcuts (SSC): rate-0 -> bits 0; rate-1 ->
+//    hard decisions of the node LLRs, taken only when a conservative bound
+//    proves no exact zero can arise inside the sub-tree (so plain SC would
+//    make the same decisions); repetition -> the g-chain tree sum in SC's own
+//    pairing order.  PQ_OPT_SSC=0 disables all of them.
+//  * f uses only IEEE add/mul/fma/div/rint (compiled with --fmad=false), so
+//    the fp32 oracle mirror in oracle/sc_oracle.c reproduces every stage LLR
+//    bit for bit.
+
+#include <cuda_runtime.h>
+#include <stdarg.h>
+#include <stdint.h>
+#include <stdio.h>
+#include <stdlib.h>
+#include <string.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/polarsc.h"
+
+// ---------------------------------------------------------------------------
+// error plumbing
+
+static thread_local std::string g_last_error;
+
+static int set_err(int code, const char *fmt, ...) __attribute__((format(printf, 2, 3)));
+static int set_err(int code, const char *fmt, ...)
+{
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_last_error = buf;
+    return code;
+}
+
+#define CUDA_TRY(expr)                                                                      \
+    do {                                                                                    \
+        cudaError_t e_ = (expr);                                                            \
+        if (e_ != cudaSuccess)                                                              \
+            return set_err(1 + (int)e_, "%s failed: %s", #expr, cudaGetErrorString(e_)); \
+    } while (0)
+
+// ---------------------------------------------------------------------------
+// device math: the exact boxplus in IEEE-only fp32 (mirrored by
+// oracle/sc_oracle.c:orc_fmag_f32; the two must agree bit for bit)
+
+#define LN2_HI 0.693145751953125f
+#define LN2_LO 1.42860682030941723212e-6f
+#define INV_LN2 1.44269504088896341f
+
+// e = e^-x, m = 1 - e^-x for x >= 0: Cody-Waite reduction, Taylor-7 expm1
+__device__ __forceinline__ void pq_expm(float x, float &e, float &m)
+{
+    x = x > 100.0f ? 100.0f : x;
+    const float kf = rintf(x * INV_LN2);
+    float r = fmaf(-kf, LN2_HI, x);
+    r = fmaf(-kf, LN2_LO, r);
+    const float t = -r;
+    float h = fmaf(t, 1.0f / 40320.0f, 1.0f / 5040.0f);
+    h = fmaf(t, h, 1.0f / 720.0f);
+    h = fmaf(t, h, 1.0f / 120.0f);
+    h = fmaf(t, h, 1.0f / 24.0f);
+    h = fmaf(t, h, 1.0f / 6.0f);
+    h = fmaf(t, h, 0.5f);
+    const float p = fmaf(t * t, h, t);
+    const int k = (int)kf;
+    if (k > 125) {
+        e = 0.0f;
+        m = 1.0f;
+    } else {
+        const float s = __uint_as_float((uint32_t)(127 - k) << 23);
+        e = fmaf(s, p, s);
+        m = fmaf(-s, p, 1.0f - s);
+    }
+}
+
+// log1p(num / den), den > 0, num/den >= -0.5
+__device__ __forceinline__ float pq_log1p_ratio(float num, float den)
+{
+    float s, kf;
+    if (num >= -0.29289322f * den && num <= 0.41421356f * den) {
+        s = num / (2.0f * den + num);
+        kf = 0.0f;
+    } else {
+        const float u = 1.0f + num / den;
+        const uint32_t b = __float_as_uint(u);
+        int k = (int)((b >> 23) & 0xffu) - 127;
+        float mm = __uint_as_float((b & 0x007fffffu) | 0x3f800000u);
+        if (mm > 1.41421356f) {
+            mm *= 0.5f;
+            k += 1;
+        }
+        s = (mm - 1.0f) / (mm + 1.0f);
+        kf = (float)k;
+    }
+    const float z = s * s;
+    float h = fmaf(z, 1.0f / 11.0f, 1.0f / 9.0f);
+    h = fmaf(z, h, 1.0f / 7.0f);
+    h = fmaf(z, h, 1.0f / 5.0f);
+    h = fmaf(z, h, 1.0f / 3.0f);
+    const float s2 = s + s;
+    const float p = fmaf(s2 * z, h, s2);
+    return fmaf(kf, LN2_HI, fmaf(kf, LN2_LO, p));
+}
+
+// |f| for magnitudes a, b >= 0:
+//   log1p((1-e^-lo)(1-e^-hi) / (e^-lo + e^-hi))     lo <= 40
+//   lo + log1p(-e / (1 + e)), e = e^-(hi-lo)        lo >  40
+// = log((1 + e^-a e^-b)/(e^-a + e^-b)) = phi(phi(a) + phi(b)),
+// the reference's stable boxplus (construction.py:300-303) without its
+// small-magnitude cancellation.
+__device__ __forceinline__ float pq_fmag(float a, float b)
+{
+    const float lo = fminf(a, b), hi = fmaxf(a, b);
+    const bool big = lo > 40.0f;
+    float e1, m1, e2, m2;
+    pq_expm(big ? hi - lo : lo, e1, m1);
+    pq_expm(hi, e2, m2);
+    const float num = big ? -e1 : m1 * m2;
+    const float den = big ? 1.0f + e1 : e1 + e2;
+    const float base = big ? lo : 0.0f;
+    return base + pq_log1p_ratio(num, den);
+}
+
+template <int FM>
+__device__ __forceinline__ float pq_f(float a, float b)
+{
+    const float ma = fabsf(a), mb = fabsf(b);
+    const float mag = FM == PQ_F_MINSUM ? fminf(ma, mb) : pq_fmag(ma, mb);
+    return __uint_as_float(__float_as_uint(mag) | ((__float_as_uint(a) ^ __float_as_uint(b)) & 0x80000000u));
+}
+
+// g(a, b, s) = b + (1 - 2s) a
+__device__ __forceinline__ float pq_g(float a, float b, uint32_t s) { return s ? b - a : b + a; }
+
+// Lower bound on |boxplus(t, t)| (exact arithmetic): 0.427 t^2 for t < 1,
+// max(0.427, t - ln 2) for t >= 1.  Chained k times from min|L| of a rate-1
+// node it lower-bounds every LLR inside the node's sub-tree (|g| >= max of its
+// operands there, boxplus is monotone), so a result >= 1e-30 proves no fp32
+// underflow to an exact zero -- the only way plain SC could decide differently
+// from the node's hard decisions.  tests/test_oracle.py checks the bound.
+__device__ __forceinline__ bool rate1_guard(float m, int k)
+{
+    float t = m;
+    for (int i = 0; i < k; i++) t = t < 1.0f ? 0.427f * t * t : fmaxf(0.427f, t - 0.6932f);
+    return t >= 1e-30f;
+}
+
+// ---------------------------------------------------------------------------
+// node types (host computes them from the frozen mask; heap order)
+
+enum : uint8_t { NT_MIXED = 0, NT_RATE0 = 1, NT_RATE1 = 2, NT_REP = 3 };
+
+struct DecParams {
+    int n, log2S, plain, frames;
+    uint32_t N, S, wpf;          // block length, shared sub-tree width, words per frame
+    const float *llr;            // [F][N] fp32 channel LLRs (or null when ybits)
+    const uint32_t *ybits;       // [F][wpf] BSC received bits (or null)
+    float mag;                   // BSC LLR magnitude
+    const uint32_t *cw;          // [F][wpf] coset words c = T(v & mask), or null
+    const uint8_t *types;        // [2N] heap-order node types
+    float *scr;                  // [F][N] stage buffers for widths > S
+    uint32_t *X;                 // [F][wpf] out: shifted x-hat partial sums
+    float *dump;                 // [F][n+1][N] stage dump (plain mode), or null
+};
+
+struct FrameCtx {
+    const float *llr;
+    const uint32_t *y, *cw;
+    float *scr;
+    uint32_t *X;
+    float *dump;
+};
+
+__device__ __forceinline__ float chan_load(const DecParams &p, const FrameCtx &fc, uint32_t i)
+{
+    uint32_t c = fc.cw ? (fc.cw[i >> 5] >> (i & 31)) & 1u : 0u;
+    if (fc.y) {
+        const uint32_t y = (fc.y[i >> 5] >> (i & 31)) & 1u;
+        return (y ^ c) ? -p.mag : p.mag;
+    }
+    const float v = fc.llr[i];
+    return c ? -v : v;
+}
+
+// smem layout: [2S floats stage LLRs][SW words partial sums][2S bytes types]
+struct Smem {
+    float *st;
+    uint32_t *xs;
+    uint8_t *ty;
+};
+
+// stage pointer for a node of width W at depth d >= 1
+__device__ __forceinline__ float *stage_ptr(const DecParams &p, const FrameCtx &fc, const Smem &sm,
+                                            uint32_t W)
+{
+    return W <= p.S ? sm.st + (2 * p.S - 2 * W) : fc.scr + (p.N - 2 * W);
+}
+
+// ---------------------------------------------------------------------------
+// warp-level sub-tree decoder, W <= 64, LLRs in registers:
+// W <= 32: lane l holds element l in v0;  W == 64: v0 = element l, v1 = element l+32.
+// Returns the node's W partial-sum bits (uniform across the warp).
+
+struct WarpCtx {
+    const uint8_t *ty;   // local heap types of the current S-sub-tree (smem)
+    float *dump;         // frame dump base or null
+    uint32_t N;
+    int plain;
+};
+
+template <int W, int FM>
+__device__ __noinline__ uint64_t wdec(float v0, float v1, int lh, const WarpCtx &c, int d, uint32_t j)
+{
+    const int lane = threadIdx.x & 31;
+    const uint8_t t = c.ty[lh];
+    if (t == NT_RATE0 && (W == 1 || !c.plain)) return 0;
+    if constexpr (W == 1) {
+        const float L = __shfl_sync(0xffffffffu, v0, 0);
+        return L < 0.0f ? 1ull : 0ull;
+    } else {
+        constexpr int H = W / 2;
+        constexpr uint64_t FULLW = W == 64 ? ~0ull : ((1ull << W) - 1);
+        if (!c.plain && t == NT_RATE1) {
+            uint32_t m = lane < W ? (__float_as_uint(v0) & 0x7fffffffu) : 0x7f800000u;
+            if (W == 64) m = min(m, __float_as_uint(v1) & 0x7fffffffu);
+            m = __reduce_min_sync(0xffffffffu, m);
+            int k = 0;
+            for (int w = W; w > 1; w >>= 1) k++;
+            if (rate1_guard(__uint_as_float(m), k)) {
+                uint64_t bits = __ballot_sync(0xffffffffu, v0 < 0.0f);
+                if (W == 64) bits |= (uint64_t)__ballot_sync(0xffffffffu, v1 < 0.0f) << 32;
+                return bits & FULLW;
+            }
+        }
+        if (!c.plain && t == NT_REP) {
+            // last-leaf LLR of a repetition node = SC's g-chain with zero partial
+            // sums, summed in SC's own pairing order (r_i = L[i+w/2] + L[i])
+            float s = W == 64 ? v1 + v0 : v0;
+            for (int h = (W == 64 ? 16 : H); h >= 1; h >>= 1) {
+                const float o = __shfl_down_sync(0xffffffffu, s, h);
+                s = o + s;
+            }
+            const float L = __shfl_sync(0xffffffffu, s, 0);
+            return L < 0.0f ? FULLW : 0ull;
+        }
+        float a, b;
+        if (W == 64) {
+            a = v0;
+            b = v1;
+        } else {
+            a = v0;
+            b = __shfl_down_sync(0xffffffffu, v0, H);
+        }
+        uint64_t xl = 0;
+        const bool skipl = !c.plain && c.ty[2 * lh] == NT_RATE0;
+        if (!skipl) {
+            const float fl = pq_f<FM>(a, b);
+            if (c.dump && lane < H) c.dump[(size_t)(d + 1) * c.N + (size_t)(2 * j) * H + lane] = fl;
+            xl = wdec<H, FM>(fl, 0.0f, 2 * lh, c, d + 1, 2 * j);
+        }
+        uint64_t xr = 0;
+        const bool skipr = !c.plain && c.ty[2 * lh + 1] == NT_RATE0;
+        if (!skipr) {
+            const uint32_t s = (uint32_t)(xl >> lane) & 1u;
+            const float gr = pq_g(a, b, s);
+            if (c.dump && lane < H) c.dump[(size_t)(d + 1) * c.N + (size_t)(2 * j + 1) * H + lane] = gr;
+            xr = wdec<H, FM>(gr, 0.0f, 2 * lh + 1, c, d + 1, 2 * j + 1);
+        }
+        return (xl ^ xr) | (xr << H);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// bit-range helpers on packed partial sums
+
+// write W (<= 64) bits at bit position pos of word array x (single thread)
+__device__ __forceinline__ void put_bits(uint32_t *x, uint32_t pos, uint32_t W, uint64_t bits)
+{
+    if (W >= 32) {
+        x[pos >> 5] = (uint32_t)bits;
+        if (W == 64) x[(pos >> 5) + 1] = (uint32_t)(bits >> 32);
+    } else {
+        const uint32_t sh = pos & 31, m = ((1u << W) - 1u) << sh;
+        uint32_t *w = x + (pos >> 5);
+        *w = (*w & ~m) | (((uint32_t)bits << sh) & m);
+    }
+}
+
+__device__ __forceinline__ uint32_t get_bit(const uint32_t *x, uint32_t pos) { return (x[pos >> 5] >> (pos & 31)) & 1u; }
+
+// block-wide: zero W bits at pos (W >= 32: word aligned)
+__device__ __forceinline__ void zero_bits_block(uint32_t *x, uint32_t pos, uint32_t W)
+{
+    if (W < 32) {
+        if (threadIdx.x == 0) put_bits(x, pos, W, 0);
+        return;
+    }
+    for (uint32_t w = threadIdx.x; w < W / 32; w += blockDim.x) x[(pos >> 5) + w] = 0;
+}
+
+// block-wide: bits[lpos .. lpos+W) ^= bits[lpos+W .. lpos+2W)
+__device__ __forceinline__ void combine_block(uint32_t *x, uint32_t lpos, uint32_t W)
+{
+    if (W < 32) {
+        if (threadIdx.x == 0) {
+            uint32_t *w = x + (lpos >> 5);
+            const uint32_t sh = lpos & 31, m = (1u << W) - 1u;
+            const uint32_t r = (*w >> (sh + W)) & m;
+            *w ^= r << sh;
+        }
+        return;
+    }
+    const uint32_t nw = W / 32, b = lpos >> 5;
+    for (uint32_t w = threadIdx.x; w < nw; w += blockDim.x) x[b + w] ^= x[b + nw + w];
+}
+
+__device__ __forceinline__ float block_min(float v, float *red)
+{
+    uint32_t m = __float_as_uint(v);
+    m = __reduce_min_sync(0xffffffffu, m);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+    __syncthreads();
+    if (lane == 0) ((uint32_t *)red)[warp] = m;
+    __syncthreads();
+    uint32_t r = lane < nw ? ((uint32_t *)red)[lane] : 0x7f800000u;
+    r = __reduce_min_sync(0xffffffffu, r);
+    return __uint_as_float(r);
+}
+
+// ---------------------------------------------------------------------------
+// the per-frame tree walk
+
+template <int W, int FM>
+__device__ __forceinline__ uint64_t warp_entry(const float *src, bool chan, const DecParams &p,
+                                               const FrameCtx &fc, int lh, const WarpCtx &wc, int d,
+                                               uint32_t j)
+{
+    const int lane = threadIdx.x & 31;
+    float v0 = 0.0f, v1 = 0.0f;
+    if (chan) {
+        if (lane < W) v0 = chan_load(p, fc, lane);
+        if (W == 64) v1 = chan_load(p, fc, 32 + lane);
+    } else {
+        if (lane < W) v0 = src[lane];
+        if (W == 64) v1 = src[32 + lane];
+    }
+    return wdec<W, FM>(v0, v1, lh, wc, d, j);
+}
+
+template <int FM>
+__global__ void __launch_bounds__(256) sc_decode_kernel(DecParams p)
+{
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    __shared__ float red[32];
+    const uint32_t S = p.S, N = p.N;
+    Smem sm;
+    sm.st = (float *)smem_raw;
+    sm.xs = (uint32_t *)(sm.st + 2 * S);
+    const uint32_t SW = S >= 32 ? S / 32 : 1;
+    sm.ty = (uint8_t *)(sm.xs + SW);
+
+    const uint32_t frame = blockIdx.x;
+    FrameCtx fc;
+    fc.llr = p.llr ? p.llr + (size_t)frame * N : nullptr;
+    fc.y = p.ybits ? p.ybits + (size_t)frame * p.wpf : nullptr;
+    fc.cw = p.cw ? p.cw + (size_t)frame * p.wpf : nullptr;
+    fc.scr = p.scr ? p.scr + (size_t)frame * N : nullptr;
+    fc.X = p.X + (size_t)frame * p.wpf;
+    fc.dump = p.dump ? p.dump + (size_t)frame * (p.n + 1) * N : nullptr;
+
+    WarpCtx wc;
+    wc.ty = sm.ty;
+    wc.dump = fc.dump;
+    wc.N = N;
+    wc.plain = p.plain;
+
+    const int tid = threadIdx.x, nthr = blockDim.x;
+    const int dS = p.n - p.log2S;  // depth of the shared-memory sub-tree roots
+
+    if (fc.dump)
+        for (uint32_t i = tid; i < N; i += nthr) fc.dump[i] = chan_load(p, fc, i);
+
+    // type of node (d, j): nodes strictly inside the loaded sub-tree come from
+    // shared memory, everything else from the global heap-order table
+    auto ntype = [&](int d, uint32_t j) -> uint8_t {
+        const uint32_t W = N >> d;
+        uint8_t t;
+        if (W < S) {
+            const int e = d - dS;
+            t = sm.ty[(1u << e) + (j & ((1u << e) - 1u))];
+        } else {
+            t = __ldg(p.types + ((size_t)1 << d) + j);
+        }
+        return t;
+    };
+    auto xptr = [&](uint32_t W) -> uint32_t * { return W <= S ? sm.xs : fc.X; };
+    auto xpos = [&](uint32_t W, uint32_t pos) -> uint32_t { return W <= S ? (pos & (S - 1)) : pos; };
+
+    int d = 0;
+    uint32_t j = 0;
+    bool entering = true;
+    for (;;) {
+        const uint32_t W = N >> d;
+        if (entering) {
+            uint8_t t = ntype(d, j);
+            if (p.plain && W > 1) t = NT_MIXED;
+            if (t == NT_RATE0) {
+                __syncthreads();
+                zero_bits_block(xptr(W), xpos(W, j * W), W);
+                entering = false;
+                continue;
+            }
+            if (W == S) {
+                // entering a shared-memory sub-tree: stage its node types
+                __syncthreads();
+                for (uint32_t q = 1 + tid; q < 2 * S; q += nthr) {
+                    const int e = 31 - __clz(q);
+                    sm.ty[q] = __ldg(p.types + ((size_t)1 << (dS + e)) + ((size_t)j << e) + (q - (1u << e)));
+                }
+            }
+            if (W <= 64) {
+                __syncthreads();
+                if (tid < 32) {
+                    const bool chan = d == 0;
+                    const float *src = chan ? nullptr : stage_ptr(p, fc, sm, W);
+                    const int e = d - dS;
+                    const int lh = (1 << e) + (int)(j & ((1u << e) - 1u));
+                    uint64_t bits;
+                    switch (W) {
+                    case 64: bits = warp_entry<64, FM>(src, chan, p, fc, lh, wc, d, j); break;
+                    case 32: bits = warp_entry<32, FM>(src, chan, p, fc, lh, wc, d, j); break;
+                    case 16: bits = warp_entry<16, FM>(src, chan, p, fc, lh, wc, d, j); break;
+                    case 8: bits = warp_entry<8, FM>(src, chan, p, fc, lh, wc, d, j); break;
+                    case 4: bits = warp_entry<4, FM>(src, chan, p, fc, lh, wc, d, j); break;
+                    case 2: bits = warp_entry<2, FM>(src, chan, p, fc, lh, wc, d, j); break;
+                    default: bits = warp_entry<1, FM>(src, chan, p, fc, lh, wc, d, j); break;
+                    }
+                    if (tid == 0) put_bits(sm.xs, (j * W) & (S - 1), W, bits);
+                }
+                entering = false;
+                continue;
+            }
+            const float *src = d == 0 ? nullptr : stage_ptr(p, fc, sm, W);
+            if (t == NT_RATE1 && !p.plain) {
+                __syncthreads();
+                float m = __int_as_float(0x7f800000);
+                for (uint32_t i = tid; i < W; i += nthr) {
+                    const float v = d == 0 ? chan_load(p, fc, i) : src[i];
+                    m = fminf(m, fabsf(v));
+                }
+                m = block_min(m, red);
+                int k = 0;
+                for (uint32_t w = W; w > 1; w >>= 1) k++;
+                if (rate1_guard(m, k)) {
+                    uint32_t *xb = xptr(W);
+                    const uint32_t base = xpos(W, j * W) >> 5;
+                    for (uint32_t i0 = 0; i0 < W; i0 += nthr) {
+                        const uint32_t i = i0 + tid;
+                        const float v = i < W ? (d == 0 ? chan_load(p, fc, i) : src[i]) : 0.0f;
+                        const uint32_t bits = __ballot_sync(0xffffffffu, v < 0.0f);
+                        if ((tid & 31) == 0 && i < W) xb[base + (i >> 5)] = bits;
+                    }
+                    entering = false;
+                    continue;
+                }
+            }
+            // mixed node: f-step into the left child unless it is rate-0
+            const uint32_t H = W / 2;
+            const uint8_t tl = p.plain ? NT_MIXED : ntype(d + 1, 2 * j);
+            __syncthreads();
+            if (tl == NT_RATE0) {
+                zero_bits_block(xptr(H), xpos(H, 2 * j * H), H);
+                d++;
+                j = 2 * j;
+                entering = false;
+                continue;
+            }
+            float *dst = stage_ptr(p, fc, sm, H);
+            float *dmp = fc.dump ? fc.dump + (size_t)(d + 1) * N + (size_t)(2 * j) * H : nullptr;
+            for (uint32_t i = tid; i < H; i += nthr) {
+                const float a = d == 0 ? chan_load(p, fc, i) : src[i];
+                const float b = d == 0 ? chan_load(p, fc, i + H) : src[i + H];
+                const float v = pq_f<FM>(a, b);
+                dst[i] = v;
+                if (dmp) dmp[i] = v;
+            }
+            d++;
+            j = 2 * j;
+            continue;
+        }
+        // ---- node (d, j) is decided; its partial sums are in place
+        if (W == S && S < N) {
+            __syncthreads();
+            for (uint32_t w = tid; w < S / 32; w += nthr) fc.X[(j * S) / 32 + w] = sm.xs[w];
+        }
+        if (d == 0) {
+            if (S >= N) {
+                __syncthreads();
+                if (N >= 32) {
+                    for (uint32_t w = tid; w < N / 32; w += nthr) fc.X[w] = sm.xs[w];
+                } else if (tid == 0) {
+                    fc.X[0] = sm.xs[0] & ((1u << N) - 1u);
+                }
+            }
+            break;
+        }
+        if ((j & 1) == 0) {
+            // left child done -> g-step at the parent into the right child
+            const uint32_t jr = j + 1;
+            const uint8_t tr = p.plain ? NT_MIXED : ntype(d, jr);
+            __syncthreads();
+            if (tr == NT_RATE0) {
+                zero_bits_block(xptr(W), xpos(W, jr * W), W);
+                j = jr;
+                continue;  // still exiting: the right child is decided
+            }
+            const uint32_t W2 = 2 * W;
+            const float *src = d - 1 == 0 ? nullptr : stage_ptr(p, fc, sm, W2);
+            const uint32_t *xl = xptr(W);
+            const uint32_t lpos = xpos(W, j * W);
+            float *dst = stage_ptr(p, fc, sm, W);
+            float *dmp = fc.dump ? fc.dump + (size_t)d * N + (size_t)jr * W : nullptr;
+            for (uint32_t i = tid; i < W; i += nthr) {
+                const float a = d - 1 == 0 ? chan_load(p, fc, i) : src[i];
+                const float b = d - 1 == 0 ? chan_load(p, fc, i + W) : src[i + W];
+                const float v = pq_g(a, b, get_bit(xl, lpos + i));
+                dst[i] = v;
+                if (dmp) dmp[i] = v;
+            }
+            j = jr;
+            entering = true;
+            continue;
+        }
+        // right child done -> parent's partial sums = (xl ^ xr, xr)
+        __syncthreads();
+        combine_block(xptr(2 * W), xpos(2 * W, (j - 1) * W), W);
+        d--;
+        j >>= 1;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// polar transform on packed frames (XOR butterflies)
+// x = u F^{(x)n}: for h = 1, 2, ..., N/2 and i with (i & h) == 0: v[i] ^= v[i+h]
+// Pass 1: within a tile of TW <= 1024 words (intra-word stages by mask/shift,
+// cross-word stages in shared memory).  Pass 2: the remaining stages across
+// tiles, as a column transform with row stride TW.
+
+__device__ __forceinline__ uint32_t intra_word_transform(uint32_t v, uint32_t nbits)
+{
+    if (nbits > 1) v ^= (v >> 1) & 0x55555555u;
+    if (nbits > 2) v ^= (v >> 2) & 0x33333333u;
+    if (nbits > 4) v ^= (v >> 4) & 0x0f0f0f0fu;
+    if (nbits > 8) v ^= (v >> 8) & 0x00ff00ffu;
+    if (nbits > 16) v ^= (v >> 16) & 0x0000ffffu;
+    return v;
+}
+
+struct XfParams {
+    const uint32_t *in;
+    uint32_t *out;
+    const uint32_t *and_mask;  // [wpf] applied on load (shared by frames), or null
+    const uint32_t *xor_post;  // [F][wpf] XORed into the output of the final pass, or null
+    uint32_t wpf, TW, nbits_word;
+    int final_pass;
+};
+
+__global__ void __launch_bounds__(256) xf_pass1(XfParams p)
+{
+    extern __shared__ uint32_t tile[];
+    const uint32_t tiles_per_frame = p.wpf / p.TW;
+    const uint32_t frame = blockIdx.x / tiles_per_frame, t = blockIdx.x % tiles_per_frame;
+    const size_t base = (size_t)frame * p.wpf + (size_t)t * p.TW;
+    for (uint32_t w = threadIdx.x; w < p.TW; w += blockDim.x) {
+        uint32_t v = p.in[base + w];
+        if (p.and_mask) v &= p.and_mask[t * p.TW + w];
+        tile[w] = intra_word_transform(v, p.nbits_word);
+    }
+    for (uint32_t h = 1; h < p.TW; h <<= 1) {
+        __syncthreads();
+        for (uint32_t w = threadIdx.x; w < p.TW; w += blockDim.x)
+            if ((w & h) == 0) tile[w] ^= tile[w + h];
+    }
+    __syncthreads();
+    for (uint32_t w = threadIdx.x; w < p.TW; w += blockDim.x) {
+        uint32_t v = tile[w];
+        if (p.nbits_word < 32) v &= (1u << p.nbits_word) - 1u;
+        if (p.final_pass && p.xor_post) v ^= p.xor_post[base + w];
+        p.out[base + w] = v;
+    }
+}
+
+// rows R = wpf / TW; each CTA owns 32 adjacent columns of one frame
+__global__ void __launch_bounds__(256) xf_pass2(XfParams p)
+{
+    extern __shared__ uint32_t colbuf[];  // [R][32]
+    const uint32_t R = p.wpf / p.TW, cgroups = p.TW / 32;
+    const uint32_t frame = blockIdx.x / cgroups, cg = blockIdx.x % cgroups;
+    const size_t fbase = (size_t)frame * p.wpf + (size_t)cg * 32;
+    const uint32_t lane = threadIdx.x & 31, rw = threadIdx.x >> 5, nrw = blockDim.x >> 5;
+    for (uint32_t r = rw; r < R; r += nrw) colbuf[r * 32 + lane] = p.out[fbase + (size_t)r * p.TW + lane];
+    for (uint32_t h = 1; h < R; h <<= 1) {
+        __syncthreads();
+        for (uint32_t r = rw; r < R; r += nrw)
+            if ((r & h) == 0) colbuf[r * 32 + lane] ^= colbuf[(r + h) * 32 + lane];
+    }
+    __syncthreads();
+    for (uint32_t r = rw; r < R; r += nrw) {
+        uint32_t v = colbuf[r * 32 + lane];
+        if (p.xor_post) v ^= p.xor_post[fbase + (size_t)r * p.TW + lane];
+        p.out[fbase + (size_t)r * p.TW + lane] = v;
+    }
+}
+
+__global__ void xor_words(const uint32_t *a, const uint32_t *b, uint32_t *out, size_t nwords)
+{
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < nwords; i += (size_t)gridDim.x * blockDim.x)
+        out[i] = a[i] ^ b[i];
+}
+
+__global__ void xor_masked(uint32_t *u, const uint32_t *v, const uint32_t *mask, uint32_t wpf, size_t nwords)
+{
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < nwords; i += (size_t)gridDim.x * blockDim.x)
+        u[i] ^= v[i] & mask[i % wpf];
+}
+
+static int launch_transform(const uint32_t *in, uint32_t *out, int n, int frames, const uint32_t *and_mask,
+                            const uint32_t *xor_post, cudaStream_t st, int *launches)
+{
+    const uint32_t N = 1u << n;
+    const uint32_t wpf = N >= 32 ? N / 32 : 1;
+    XfParams p;
+    p.in = in;
+    p.out = out;
+    p.and_mask = and_mask;
+    p.xor_post = xor_post;
+    p.wpf = wpf;
+    p.TW = wpf < 1024 ? wpf : 1024;
+    p.nbits_word = N >= 32 ? 32 : N;
+    const bool two = wpf > p.TW;
+    p.final_pass = two ? 0 : 1;
+    const uint32_t tiles = wpf / p.TW;
+    xf_pass1<<<(unsigned)(frames * tiles), 256, p.TW * 4, st>>>(p);
+    CUDA_TRY(cudaGetLastError());
+    (*launches)++;
+    if (two) {
+        const uint32_t R = wpf / p.TW;
+        const size_t smem = (size_t)R * 32 * 4;
+        if (smem > 227 * 1024) return set_err(-1, "polar transform: n=%d too large", n);
+        CUDA_TRY(cudaFuncSetAttribute(xf_pass2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        p.in = out;
+        p.final_pass = 1;
+        xf_pass2<<<(unsigned)(frames * (p.TW / 32)), 256, smem, st>>>(p);
+        CUDA_TRY(cudaGetLastError());
+        (*launches)++;
+    }
+    return 0;
+}
+
+// ---------------------------------------------------------------------------
+// host side
+
+struct pq_decoder {
+    int n, max_frames, fmode, device, ssc, log2S_opt;
+    uint32_t N, wpf;
+    int have_mask;
+    int sm_count;
+    uint8_t *d_types;
+    uint32_t *d_mask;
+    uint32_t *d_cw;
+    uint32_t *d_x;
+    float *d_scr;
+    size_t scr_elems;
+    size_t ws_bytes;
+    int last_launches;
+};
+
+static int choose_log2S(const pq_decoder *h, int frames)
+{
+    const int lo = h->n < 6 ? h->n : 6;  // warp sub-trees (W <= 64) must sit inside S
+    if (h->log2S_opt > 0) {
+        int k = h->log2S_opt < h->n ? h->log2S_opt : h->n;
+        return k < lo ? lo : k;
+    }
+    const int per_sm = (frames + h->sm_count - 1) / h->sm_count;
+    int best = 6;
+    for (int k = 6; k <= 14; k++) {
+        const size_t S = (size_t)1 << k;
+        const size_t bytes = 8 * S + (S / 32) * 4 + 2 * S;
+        if ((size_t)per_sm * bytes <= 200 * 1024) best = k;
+    }
+    if (best > h->n) best = h->n;
+    return best;
+}
+
+static size_t dec_smem_bytes(uint32_t S)
+{
+    const uint32_t SW = S >= 32 ? S / 32 : 1;
+    return (size_t)8 * S + (size_t)SW * 4 + (size_t)2 * S;
+}
+
+extern "C" {
+
+const char *pq_last_error(void) { return g_last_error.c_str(); }
+int pq_abi_version(void) { return PQ_ABI_VERSION; }
+
+int pq_decoder_create(pq_decoder **out, int n, int max_frames, int f_mode, int device)
+{
+    if (!out) return set_err(-1, "out is NULL");
+    *out = nullptr;
+    if (n < 1 || n > 25) return set_err(-1, "n must be in [1, 25], got %d", n);
+    if (max_frames < 1) return set_err(-1, "max_frames must be >= 1, got %d", max_frames);
+    if (f_mode != PQ_F_EXACT && f_mode != PQ_F_MINSUM) return set_err(-1, "unknown f mode %d", f_mode);
+    CUDA_TRY(cudaSetDevice(device));
+    pq_decoder *h = new pq_decoder();
+    h->n = n;
+    h->max_frames = max_frames;
+    h->fmode = f_mode;
+    h->device = device;
+    h->ssc = 1;
+    h->log2S_opt = 0;
+    h->N = 1u << n;
+    h->wpf = h->N >= 32 ? h->N / 32 : 1;
+    cudaDeviceProp prop;
+    cudaError_t e = cudaGetDeviceProperties(&prop, device);
+    if (e != cudaSuccess) {
+        delete h;
+        return set_err(1 + (int)e, "cudaGetDeviceProperties: %s", cudaGetErrorString(e));
+    }
+    h->sm_count = prop.multiProcessorCount;
+    const size_t wbytes = (size_t)max_frames * h->wpf * 4;
+    h->scr_elems = (size_t)max_frames * h->N;
+    size_t total = 0;
+#define ALLOC(ptr, bytes)                                                                  \
+    do {                                                                                   \
+        e = cudaMalloc((void **)&(ptr), (bytes));                                          \
+        if (e != cudaSuccess) {                                                            \
+            pq_decoder_destroy(h);                                                         \
+            return set_err(1 + (int)e, "cudaMalloc(%zu): %s", (size_t)(bytes), cudaGetErrorString(e)); \
+        }                                                                                  \
+        total += (bytes);                                                                  \
+    } while (0)
+    ALLOC(h->d_types, (size_t)2 * h->N);
+    ALLOC(h->d_mask, (size_t)h->wpf * 4);
+    ALLOC(h->d_cw, wbytes);
+    ALLOC(h->d_x, wbytes);
+    ALLOC(h->d_scr, h->scr_elems * 4);
+#undef ALLOC
+    h->ws_bytes = total;
+    *out = h;
+    return 0;
+}
+
+int pq_decoder_destroy(pq_decoder *h)
+{
+    if (!h) return 0;
+    cudaFree(h->d_types);
+    cudaFree(h->d_mask);
+    cudaFree(h->d_cw);
+    cudaFree(h->d_x);
+    cudaFree(h->d_scr);
+    delete h;
+    return 0;
+}
+
+size_t pq_decoder_workspace_bytes(const pq_decoder *h) { return h ? h->ws_bytes : 0; }
+int pq_decoder_last_launches(const pq_decoder *h) { return h ? h->last_launches : 0; }
+
+int pq_decoder_set_option(pq_decoder *h, int key, int value)
+{
+    if (!h) return set_err(-1, "handle is NULL");
+    switch (key) {
+    case PQ_OPT_SSC: h->ssc = value ? 1 : 0; return 0;
+    case PQ_OPT_SUBTREE_LOG2:
+        if (value != 0 && (value < 1 || value > 14)) return set_err(-1, "subtree log2 must be 0 or 1..14");
+        h->log2S_opt = value;
+        return 0;
+    case PQ_OPT_FMODE:
+        if (value != PQ_F_EXACT && value != PQ_F_MINSUM) return set_err(-1, "unknown f mode %d", value);
+        h->fmode = value;
+        return 0;
+    default: return set_err(-1, "unknown option %d", key);
+    }
+}
+
+int pq_decoder_get_option(const pq_decoder *h, int key)
+{
+    if (!h) return set_err(-1, "handle is NULL");
+    switch (key) {
+    case PQ_OPT_SSC: return h->ssc;
+    case PQ_OPT_SUBTREE_LOG2: return h->log2S_opt;
+    case PQ_OPT_FMODE: return h->fmode;
+    default: return set_err(-1, "unknown option %d", key);
+    }
+}
+
+int pq_decoder_set_frozen_mask(pq_decoder *h, const uint8_t *mask)
+{
+    if (!h || !mask) return set_err(-1, "NULL argument");
+    const uint32_t N = h->N;
+    // node types, heap order: index (1 << d) + j for node j at depth d
+    std::vector<uint8_t> ty(2 * (size_t)N, NT_MIXED);
+    std::vector<uint32_t> nfrozen(2 * (size_t)N);
+    std::vector<uint8_t> lastinfo(2 * (size_t)N);
+    for (uint32_t i = 0; i < N; i++) {
+        if (mask[i] > 1) return set_err(-1, "frozen mask entries must be 0 or 1 (index %u)", i);
+        const size_t q = N + i;
+        nfrozen[q] = mask[i];
+        lastinfo[q] = mask[i] ? 0 : 1;
+        ty[q] = mask[i] ? NT_RATE0 : NT_RATE1;
+    }
+    for (size_t q = N - 1; q >= 1; q--) {
+        const size_t l = 2 * q, r = 2 * q + 1;
+        const uint32_t W = (uint32_t)(N >> (31 - __builtin_clz((uint32_t)q)));
+        nfrozen[q] = nfrozen[l] + nfrozen[r];
+        lastinfo[q] = lastinfo[r];
+        if (nfrozen[q] == W) ty[q] = NT_RATE0;
+        else if (nfrozen[q] == 0) ty[q] = NT_RATE1;
+        else if (nfrozen[q] == W - 1 && lastinfo[q]) ty[q] = NT_REP;
+        else ty[q] = NT_MIXED;
+    }
+    ty[0] = NT_MIXED;
+    std::vector<uint32_t> words(h->wpf, 0);
+    for (uint32_t i = 0; i < N; i++)
+        if (mask[i]) words[i >> 5] |= 1u << (i & 31);
+    CUDA_TRY(cudaSetDevice(h->device));
+    CUDA_TRY(cudaMemcpy(h->d_types, ty.data(), ty.size(), cudaMemcpyHostToDevice));
+    CUDA_TRY(cudaMemcpy(h->d_mask, words.data(), words.size() * 4, cudaMemcpyHostToDevice));
+    h->have_mask = 1;
+    return 0;
+}
+
+int pq_polar_transform(const uint32_t *in, uint32_t *out, int n, int frames, void *stream)
+{
+    if (!in || !out) return set_err(-1, "NULL pointer");
+    if (n < 1 || n > 25) return set_err(-1, "n must be in [1, 25], got %d", n);
+    if (frames < 0) return set_err(-1, "frames must be >= 0");
+    if (frames == 0) return 0;
+    int launches = 0;
+    return launch_transform(in, out, n, frames, nullptr, nullptr, (cudaStream_t)stream, &launches);
+}
+
+static int decode_impl(pq_decoder *h, const float *llr, const uint32_t *ybits, float mag,
+                       const uint32_t *frozen_u, uint32_t *u_hat, uint32_t *x_hat, float *dump,
+                       int frames, void *stream)
+{
+    if (!h) return set_err(-1, "handle is NULL");
+    if (!h->have_mask) return set_err(-1, "frozen mask not set (pq_decoder_set_frozen_mask)");
+    if (frames < 0 || frames > h->max_frames)
+        return set_err(-1, "frames=%d outside [0, max_frames=%d]", frames, h->max_frames);
+    if (!llr && !ybits) return set_err(-1, "no channel input");
+    if (frames == 0) return 0;
+    cudaStream_t st = (cudaStream_t)stream;
+    CUDA_TRY(cudaSetDevice(h->device));
+    int launches = 0;
+    const uint32_t *cw = nullptr;
+    if (frozen_u) {
+        int rc = launch_transform(frozen_u, h->d_cw, h->n, frames, h->d_mask, nullptr, st, &launches);
+        if (rc) return rc;
+        cw = h->d_cw;
+    }
+    DecParams p;
+    memset(&p, 0, sizeof p);
+    p.n = h->n;
+    p.log2S = choose_log2S(h, frames);
+    p.plain = (dump || !h->ssc) ? 1 : 0;
+    p.frames = frames;
+    p.N = h->N;
+    p.S = 1u << p.log2S;
+    p.wpf = h->wpf;
+    p.llr = llr;
+    p.ybits = ybits;
+    p.mag = mag;
+    p.cw = cw;
+    p.types = h->d_types;
+    p.scr = h->d_scr;
+    p.X = h->d_x;
+    p.dump = dump;
+    const size_t smem = dec_smem_bytes(p.S);
+    if (h->fmode == PQ_F_MINSUM) {
+        CUDA_TRY(cudaFuncSetAttribute(sc_decode_kernel<PQ_F_MINSUM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)smem));
+        sc_decode_kernel<PQ_F_MINSUM><<<frames, 256, smem, st>>>(p);
+    } else {
+        CUDA_TRY(cudaFuncSetAttribute(sc_decode_kernel<PQ_F_EXACT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)smem));
+        sc_decode_kernel<PQ_F_EXACT><<<frames, 256, smem, st>>>(p);
+    }
+    CUDA_TRY(cudaGetLastError());
+    launches++;
+    const size_t nwords = (size_t)frames * h->wpf;
+    if (x_hat) {
+        if (cw) {
+            xor_words<<<(unsigned)((nwords + 255) / 256 < 4096 ? (nwords + 255) / 256 : 4096), 256, 0, st>>>(
+                h->d_x, cw, x_hat, nwords);
+            CUDA_TRY(cudaGetLastError());
+        } else {
+            CUDA_TRY(cudaMemcpyAsync(x_hat, h->d_x, nwords * 4, cudaMemcpyDeviceToDevice, st));
+        }
+        launches++;
+    }
+    if (u_hat) {
+        // u_hat = T(x_hat') XOR (v & mask): T maps the shifted partial sums back to
+        // shifted decisions (zero on the frozen set), the XOR restores the revealed values
+        int rc;
+        if (frozen_u) {
+            rc = launch_transform(h->d_x, u_hat, h->n, frames, nullptr, nullptr, st, &launches);
+            if (rc) return rc;
+            const size_t g = (nwords + 255) / 256 < 4096 ? (nwords + 255) / 256 : 4096;
+            xor_masked<<<(unsigned)g, 256, 0, st>>>(u_hat, frozen_u, h->d_mask, h->wpf, nwords);
+            CUDA_TRY(cudaGetLastError());
+            launches++;
+        } else {
+            rc = launch_transform(h->d_x, u_hat, h->n, frames, nullptr, nullptr, st, &launches);
+            if (rc) return rc;
+        }
+    }
+    h->last_launches = launches;
+    return 0;
+}
+
+int pq_sc_decode_f32(pq_decoder *h, const float *llr, const uint32_t *frozen_u, uint32_t *u_hat,
+                     uint32_t *x_hat, int frames, void *stream)
+{
+    if (!llr) return set_err(-1, "llr is NULL");
+    return decode_impl(h, llr, nullptr, 0.0f, frozen_u, u_hat, x_hat, nullptr, frames, stream);
+}
+
+int pq_sc_decode_f32_dump(pq_decoder *h, const float *llr, const uint32_t *frozen_u, uint32_t *u_hat,
+                          uint32_t *x_hat, float *dump, int frames, void *stream)
+{
+    if (!llr || !dump) return set_err(-1, "llr/dump is NULL");
+    return decode_impl(h, llr, nullptr, 0.0f, frozen_u, u_hat, x_hat, dump, frames, stream);
+}
+
+int pq_sc_decode_bsc(pq_decoder *h, const uint32_t *y_bits, float llr_mag, const uint32_t *frozen_u,
+                     uint32_t *u_hat, uint32_t *x_hat, int frames, void *stream)
+{
+    if (!y_bits) return set_err(-1, "y_bits is NULL");
+    if (!(llr_mag >= 0.0f)) return set_err(-1, "llr_mag must be >= 0");
+    return decode_impl(h, nullptr, y_bits, llr_mag, frozen_u, u_hat, x_hat, nullptr, frames, stream);
+}
+
+}  // extern "C"
+

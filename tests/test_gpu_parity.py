@@ -1,0 +1,308 @@
+"""GPU parity: the CUDA decoder (through the C ABI) against the CPU oracle.
+
+Bars (BASELINE.json north star):
+  * fp32 oracle mirror (same f, same operation order): decoded u, x and every
+    stage LLR equal -- on ALL frames, SSC or plain;
+  * f64 exact oracle: decoded bits bit-exact on every frame whose smallest
+    |decision LLR| (information positions) is >= 1e-4; stage LLRs within
+    |d| <= 1e-4 |ref| + 1e-6 on those frames;
+  * FER within the binomial 3-sigma interval of the oracle's FER.
+"""
+import numpy as np
+import pytest
+
+from conftest import golden
+from oracle import oracle as O
+from paper_1204_5882_b200 import channel as C
+from paper_1204_5882_b200 import codes as K
+from paper_1204_5882_b200.polar_core import (ScDecoder, pack_bits, polar_transform,
+                                             polar_transform_words, sc_decode, unpack_bits)
+
+pytestmark = pytest.mark.gpu
+
+
+def to_dev(a, dev):
+    import torch
+    return torch.from_numpy(np.ascontiguousarray(a)).to(dev)
+
+
+def words_dev(bits, dev):
+    return to_dev(pack_bits(bits).view(np.int32), dev)
+
+
+def from_words(t, N):
+    return unpack_bits(t.cpu().numpy().view(np.uint32), N)
+
+
+def transform_rows(v):
+    v = v.copy()
+    W = v.shape[-1]
+    h = 1
+    while h < W:
+        r = v.reshape(v.shape[:-1] + (W // (2 * h), 2, h))
+        r[..., 0, :] ^= r[..., 1, :]
+        h *= 2
+    return v
+
+
+def node_flips(mask, fz, n):
+    """Sign-flip pattern of every node's LLRs in the coset-shifted domain:
+    node (d, j) is flipped by T_W((v & mask)[jW:(j+1)W])."""
+    s = (fz & mask).astype(np.uint8)
+    N = 1 << n
+    return np.stack([transform_rows(s.reshape(1 << d, N >> d)).ravel() for d in range(n + 1)])
+
+
+def gpu_decode(dev, code, llr, fz, ssc=True, fmode="exact", want_x=True, subtree_log2=0):
+    dec = ScDecoder(code, max_frames=max(1, llr.shape[0]), f_mode=fmode, ssc=ssc,
+                    subtree_log2=subtree_log2)
+    u, x = dec.decode(to_dev(llr.astype(np.float32), dev), words_dev(fz, dev), want_x=want_x)
+    N = code.block_size
+    return from_words(u, N), (from_words(x, N) if want_x else None)
+
+
+def random_code(n, frac, rng, ch=C.BiAwgn(1.0)):
+    mask = (rng.random(1 << n) < frac).astype(np.uint8)
+    return K.PolarCode(n=n, frozen_mask=mask, channel=ch, target_fer=0.1)
+
+
+def oracle_batch(code, llr, fz, prec, fmode=O.F_EXACT, threads=8):
+    return O.sc_decode_batch(code.frozen_mask, llr.astype(np.float32), fz, precision=prec,
+                             fmode=fmode, threads=min(threads, O.max_threads()), min_info=True)
+
+
+# --------------------------------------------------------------------------
+# polar transform (K4)
+
+@pytest.mark.parametrize("n", [1, 2, 3, 4, 5, 6, 8, 10, 14, 15, 16, 17, 18, 20])
+def test_transform_bit_exact(cuda, n):
+    rng = np.random.default_rng(n)
+    F = 3 if n >= 18 else 8
+    u = rng.integers(0, 2, (F, 1 << n), dtype=np.uint8)
+    x = from_words(polar_transform_words(words_dev(u, cuda), n), 1 << n)
+    for f in range(F):
+        assert np.array_equal(x[f], O.polar_transform_bytes(u[f]))
+
+
+def test_transform_large_and_inplace(cuda):
+    n = 24
+    rng = np.random.default_rng(24)
+    u = rng.integers(0, 2, (2, 1 << n), dtype=np.uint8)
+    w = words_dev(u, cuda)
+    polar_transform_words(w, n, out=w)  # in place
+    x = from_words(w, 1 << n)
+    for f in range(2):
+        assert np.array_equal(x[f], O.polar_transform_bytes(u[f]))
+    assert np.array_equal(from_words(polar_transform_words(w, n), 1 << n), u)  # involution
+
+
+def test_transform_spec_kats(cuda):
+    assert tuple(polar_transform([0, 0, 0, 1])) == (1, 1, 1, 1)
+    assert tuple(polar_transform([1, 1, 1, 1])) == (0, 0, 0, 1)
+    assert tuple(polar_transform([0, 0, 0, 0])) == (0, 0, 0, 0)
+    with pytest.raises(ValueError):
+        polar_transform([1, 0, 1])
+
+
+# --------------------------------------------------------------------------
+# SC decode: exhaustive n = 3 (acceptance 6)
+
+@pytest.mark.parametrize("mask", [[1, 1, 1, 0, 1, 0, 0, 0], [1, 0, 1, 0, 0, 0, 0, 0], [0] * 8,
+                                  [1] * 8, [0, 1, 1, 0, 1, 0, 0, 1]])
+@pytest.mark.parametrize("ssc", [True, False])
+def test_all_256_patterns_n3(cuda, mask, ssc):
+    mask = np.array(mask, np.uint8)
+    code = K.PolarCode(n=3, frozen_mask=mask, channel=C.Bsc(0.1), target_fer=0.1)
+    y = ((np.arange(256)[:, None] >> np.arange(8)) & 1).astype(np.uint8)
+    llr = C.channel_llr(C.Bsc(0.1), y).astype(np.float32)
+    fz = np.random.default_rng(1).integers(0, 2, (256, 8)).astype(np.uint8)
+    u, x = gpu_decode(cuda, code, llr, fz, ssc=ssc)
+    for f in range(256):
+        un, _ = O.sc_decode_naive(mask, llr[f].astype(np.float64), fz[f])
+        assert np.array_equal(u[f], un), f
+        assert np.array_equal(x[f], O.polar_transform_bytes(un))
+
+
+# --------------------------------------------------------------------------
+# random codes, all sizes through every code path (warp sub-trees, shared
+# sub-trees, HBM levels), SSC and plain, exact and min-sum
+
+@pytest.mark.parametrize("n", [1, 2, 4, 5, 6, 7, 8, 10, 12, 14])
+@pytest.mark.parametrize("frac", [0.0, 0.3, 0.7, 1.0])
+def test_random_codes_vs_fp32_mirror(cuda, n, frac):
+    rng = np.random.default_rng(100 * n + int(10 * frac))
+    code = random_code(n, frac, rng)
+    F = 16
+    llr = rng.normal(0.7, 1.6, (F, 1 << n)).astype(np.float32)
+    llr[:, rng.integers(0, 1 << n, 3)] = 0.0  # exact zeros exercise the tie rule / rate-1 guard
+    fz = rng.integers(0, 2, (F, 1 << n)).astype(np.uint8)
+    ref, _ = oracle_batch(code, llr, fz, 32)
+    for ssc in (True, False):
+        u, x = gpu_decode(cuda, code, llr, fz, ssc=ssc)
+        assert np.array_equal(u, ref), f"ssc={ssc}"
+        for f in range(F):
+            assert np.array_equal(x[f], O.polar_transform_bytes(u[f]))
+
+
+@pytest.mark.parametrize("n,log2s", [(12, 7), (13, 8), (16, 10), (16, 12)])
+def test_forced_small_subtree_uses_hbm_levels(cuda, n, log2s):
+    """Small S pushes many levels into the per-frame HBM/L2 scratch path."""
+    rng = np.random.default_rng(n + log2s)
+    code = random_code(n, 0.5, rng)
+    F = 8
+    llr = rng.normal(1.0, 2.0, (F, 1 << n)).astype(np.float32)
+    fz = rng.integers(0, 2, (F, 1 << n)).astype(np.uint8)
+    ref, _ = oracle_batch(code, llr, fz, 32)
+    u, _ = gpu_decode(cuda, code, llr, fz, subtree_log2=log2s)
+    assert np.array_equal(u, ref)
+
+
+@pytest.mark.parametrize("n", [4, 8, 11])
+def test_minsum_vs_mirror(cuda, n):
+    rng = np.random.default_rng(7 + n)
+    code = random_code(n, 0.5, rng)
+    llr = rng.normal(0.5, 2.0, (12, 1 << n)).astype(np.float32)
+    fz = rng.integers(0, 2, (12, 1 << n)).astype(np.uint8)
+    ref, _ = oracle_batch(code, llr, fz, 32, fmode=O.F_MINSUM)
+    for ssc in (True, False):
+        u, _ = gpu_decode(cuda, code, llr, fz, ssc=ssc, fmode="min-sum")
+        assert np.array_equal(u, ref)
+
+
+# --------------------------------------------------------------------------
+# stage LLRs
+
+@pytest.mark.parametrize("n", [3, 6, 9, 12])
+def test_stage_dump_vs_oracles(cuda, n):
+    rng = np.random.default_rng(n)
+    code = random_code(n, 0.45, rng)
+    F = 6
+    N = 1 << n
+    llr = rng.normal(0.8, 1.8, (F, N)).astype(np.float32)
+    fz = rng.integers(0, 2, (F, N)).astype(np.uint8)
+    dec = ScDecoder(code, max_frames=F)
+    u, x, dump = dec.decode_dump(to_dev(llr, cuda), words_dev(fz, cuda))
+    dump = dump.cpu().numpy()
+    u = from_words(u, N)
+    for f in range(F):
+        sign = 1.0 - 2.0 * node_flips(code.frozen_mask, fz[f], n)
+        u32, _, st32 = O.sc_decode(code.frozen_mask, llr[f], fz[f], 32, dump=True)
+        assert np.array_equal(u[f], u32)
+        assert np.array_equal(dump[f] * sign, st32)  # every stage LLR, bit for bit (+-0 equal)
+        u64, _, st64, lf64 = O.sc_decode(code.frozen_mask, llr[f].astype(np.float64), fz[f], 64,
+                                         dump=True, leaf=True)
+        if np.min(np.abs(lf64[code.frozen_mask == 0]), initial=np.inf) >= 1e-4:
+            assert np.array_equal(u[f], u64)
+            got = dump[f].astype(np.float64) * sign
+            assert np.all(np.abs(got - st64) <= 1e-4 * np.abs(st64) + 1e-6)
+
+
+# --------------------------------------------------------------------------
+# the five BASELINE configs with the reference-constructed frozen sets
+
+CFG_FRAMES = {"c1": 64, "c2": 32, "c3": 12, "c4": 12, "c5": 2}
+
+
+def config_batch(key, frames):
+    cfg = K.CONFIGS[key]
+    code = K.load_config(key)
+    N = code.block_size
+    xs, ls = [], []
+    for j in range(frames):
+        x, y = C.frame(cfg.channel, cfg.seed, j, N)
+        xs.append(x)
+        ls.append(C.channel_llr(cfg.channel, y).astype(np.float32))
+    x = np.array(xs)
+    u = np.array([O.polar_transform_bytes(xi) for xi in xs])
+    return cfg, code, x, u, np.array(ls)
+
+
+@pytest.mark.parametrize("key", list(K.CONFIGS))
+def test_config_parity(cuda, key):
+    if key not in K.available_configs():
+        pytest.skip(f"{key}.pqct not built")
+    cfg, code, x, u_true, llr = config_batch(key, CFG_FRAMES[key])
+    ref32, _ = oracle_batch(code, llr, u_true, 32)
+    ref64, mi64 = oracle_batch(code, llr, u_true, 64)
+    u, xh = gpu_decode(cuda, code, llr, u_true)
+    assert np.array_equal(u, ref32)  # bit-exact vs the fp32 mirror on every frame
+    clean = mi64 >= 1e-4
+    assert np.array_equal(u[clean], ref64[clean])
+    ok_gpu = np.all(u == u_true, axis=1)
+    assert np.array_equal(ok_gpu, np.all(xh == x, axis=1))
+    ok64 = np.all(ref64 == u_true, axis=1)
+    F = len(ok_gpu)
+    fer, fer64 = 1 - ok_gpu.mean(), 1 - ok64.mean()
+    assert abs(fer - fer64) <= 3 * np.sqrt(max(fer64 * (1 - fer64), 1.0 / F) / F)
+    if key == "c1":
+        g = golden("c1_frames.npz")
+        assert np.array_equal(llr[:16], g["llr"])  # inputs are the reference's own
+
+
+def test_bsc_fused_front_end_matches_llr_path(cuda):
+    key = "c1" if "c1" in K.available_configs() else None
+    if key is None:
+        pytest.skip("c1 not built")
+    cfg, code, x, u_true, llr = config_batch(key, 64)
+    y = np.array([C.frame(cfg.channel, cfg.seed, j, code.block_size)[1] for j in range(64)])
+    dec = ScDecoder(code, max_frames=64)
+    u1, x1 = dec.decode(to_dev(llr, cuda), words_dev(u_true, cuda), want_x=True)
+    u2, x2 = dec.decode_bsc(words_dev(y, cuda), np.float32(cfg.channel.llr_magnitude),
+                            words_dev(u_true, cuda), want_x=True)
+    assert np.array_equal(u1.cpu().numpy(), u2.cpu().numpy())
+    assert np.array_equal(x1.cpu().numpy(), x2.cpu().numpy())
+
+
+# --------------------------------------------------------------------------
+# SPEC examples and edge cases
+
+def test_noiseless_round_trip_n10(cuda):
+    """100 random x at n=10, all LLRs +-30 -> u_hat = T(x)."""
+    rng = np.random.default_rng(10)
+    code = random_code(10, 0.3, rng)
+    x = rng.integers(0, 2, (100, 1024), dtype=np.uint8)
+    u = np.array([O.polar_transform_bytes(xi) for xi in x])
+    llr = ((1.0 - 2.0 * x) * 30.0).astype(np.float32)
+    uh, xh = gpu_decode(cuda, code, llr, u)
+    assert np.array_equal(uh, u) and np.array_equal(xh, x)
+
+
+def test_spec_sc_decode_api_single_frame(cuda):
+    rng = np.random.default_rng(4)
+    code = random_code(8, 0.5, rng, ch=C.Bsc(0.05))
+    x = rng.integers(0, 2, 256, dtype=np.uint8)
+    y = C.transmit(C.Bsc(0.05), x, 3, 1)
+    llr = C.channel_llr(C.Bsc(0.05), y)
+    u = O.polar_transform_bytes(x)
+    fv = u[code.frozen_indices()]
+    got = sc_decode(code, llr, fv)
+    ref, _ = O.sc_decode(code.frozen_mask, llr.astype(np.float32), u, 32)
+    assert np.array_equal(got, ref)
+    assert np.array_equal(got[code.frozen_indices()], fv)  # frozen positions carry the values
+    with pytest.raises(ValueError):
+        sc_decode(code, llr[:128], fv)
+    with pytest.raises(ValueError):
+        sc_decode(code, llr, fv[:-1])
+
+
+def test_argument_errors(cuda):
+    rng = np.random.default_rng(0)
+    code = random_code(6, 0.5, rng)
+    dec = ScDecoder(code, max_frames=2)
+    import torch
+    with pytest.raises(ValueError):
+        dec.decode(torch.zeros((3, 64), device=cuda))  # > max_frames
+    with pytest.raises(ValueError):
+        dec.decode(torch.zeros((2, 32), device=cuda))  # wrong N
+    u, _ = dec.decode(torch.zeros((0, 64), device=cuda))  # zero frames is a no-op
+    assert u.shape[0] == 0
+
+
+def test_ssc_equals_plain_on_large_random(cuda):
+    rng = np.random.default_rng(77)
+    code = random_code(16, 0.4, rng, ch=C.BiAwgn(1.0))
+    llr = rng.normal(1.0, 2.0, (16, 1 << 16)).astype(np.float32)
+    fz = rng.integers(0, 2, (16, 1 << 16)).astype(np.uint8)
+    a, _ = gpu_decode(cuda, code, llr, fz, ssc=True)
+    b, _ = gpu_decode(cuda, code, llr, fz, ssc=False)
+    assert np.array_equal(a, b)

@@ -1,0 +1,167 @@
+"""CPU oracle pinned against the SPEC's known answers, a brute-force SC, and
+the reference's own boxplus (golden fixture).  No GPU."""
+import numpy as np
+import pytest
+
+from conftest import golden
+from oracle import oracle as O
+
+
+# ---- polar transform KATs and invariants
+@pytest.mark.parametrize("u,x", [((0, 0, 0, 0), (0, 0, 0, 0)), ((0, 0, 0, 1), (1, 1, 1, 1)),
+                                 ((1, 1, 1, 1), (0, 0, 0, 1))])
+def test_transform_kat(u, x):
+    assert tuple(O.polar_transform_bytes(u)) == x
+    assert tuple(O.polar_transform_numpy(u)) == x
+
+
+@pytest.mark.parametrize("n", [1, 2, 4, 8, 10, 16])
+def test_transform_involution_and_two_restatements(n):
+    rng = np.random.default_rng(n)
+    for _ in range(20 if n == 16 else 200):
+        u = rng.integers(0, 2, 1 << n, dtype=np.uint8)
+        x = O.polar_transform_bytes(u)
+        assert np.array_equal(O.polar_transform_bytes(x), u)
+        if n <= 10:
+            assert np.array_equal(x, O.polar_transform_numpy(u))
+
+
+def test_transform_rejects_non_power_of_two():
+    with pytest.raises(ValueError):
+        O.polar_transform_bytes(np.zeros(6, np.uint8))
+
+
+# ---- phi
+def test_phi_kats():
+    assert abs(O.phi(2.0) - 0.2723) < 1e-3
+    assert abs(O.phi(O.phi(5.0)) - 5.0) < 1e-6
+    tab = O.phi_table()
+    assert abs(tab[512] / 256.0 - O.phi(2.0)) <= 2 ** -7  # table entry at x = 2.0
+    with pytest.raises(ValueError):
+        O.phi(0.0)
+
+
+# ---- f pinned to the reference's own boxplus (construction.py:300-303)
+def test_f64_matches_reference_boxplus():
+    g = golden("boxplus_grid.npz")
+    ours = O.fmag64(g["a"], g["b"])
+    # the reference's stable form loses relative accuracy for tiny inputs
+    # (cancellation of two log1p(~1) terms); compare absolutely there
+    tol = 1e-12 + 1e-9 * np.abs(g["f"])
+    assert np.all(np.abs(ours - g["f"]) <= np.maximum(tol, 4e-16))
+
+
+def test_f32_mirror_accuracy():
+    rng = np.random.default_rng(0)
+    for lo, hi in [(1e-7, 1e-3), (1e-3, 1.0), (1.0, 40.0), (40.0, 1e3), (1e3, 1e8), (1e-7, 1e8)]:
+        a = np.exp(rng.uniform(np.log(lo), np.log(hi), 200000)).astype(np.float32)
+        b = np.exp(rng.uniform(np.log(lo), np.log(hi), 200000)).astype(np.float32)
+        r32 = O.fmag32(a, b).astype(np.float64)
+        r64 = O.fmag64(a.astype(np.float64), b.astype(np.float64))
+        assert np.max(np.abs(r32 - r64) / r64) < 1e-6
+
+
+def test_f_identities():
+    # f(a, +inf) = a with +inf represented by the saturation value
+    a = np.array([0.1, 1.0, 3.0, 7.0])
+    assert np.allclose(O.fmag64(a, np.full(4, 30.0)), a, rtol=1e-12)
+    assert np.all(O.fmag32(np.zeros(3, np.float32), np.float32([0, 2, 50])) == 0)
+
+
+def test_rate1_guard_bound_is_a_lower_bound():
+    # the CUDA rate-1 shortcut chains b(t) <= |boxplus(t, t)|; check it here
+    t = np.geomspace(1e-20, 1e4, 20000)
+    b = np.where(t < 1.0, 0.427 * t * t, np.maximum(0.427, t - 0.6932))
+    assert np.all(b <= O.fmag64(t, t) * (1 + 1e-12))
+
+
+# ---- SC decoders: naive brute force vs C walk vs numpy recursion
+MASKS3 = [np.array(m, np.uint8) for m in ([1, 1, 1, 0, 1, 0, 0, 0], [1, 0, 1, 0, 0, 0, 0, 0],
+                                           [0] * 8, [1] * 8, [0, 1, 1, 0, 1, 0, 0, 1])]
+
+
+@pytest.mark.parametrize("mi", range(len(MASKS3)))
+def test_sc_all_256_patterns_n3(mi):
+    """SPEC.md:248 / acceptance 6: exhaustive n=3, BSC 0.1, all 256 outputs."""
+    mask = MASKS3[mi]
+    c = np.log(9.0)
+    rng = np.random.default_rng(mi)
+    for pat in range(256):
+        y = ((pat >> np.arange(8)) & 1).astype(np.uint8)
+        llr = (1 - 2 * y.astype(np.float64)) * c
+        fz = rng.integers(0, 2, 8).astype(np.uint8)
+        u_naive, leaf = O.sc_decode_naive(mask, llr, fz)
+        u64, x64, st = O.sc_decode(mask, llr, fz, 64, dump=True)
+        u32, x32 = O.sc_decode(mask, llr.astype(np.float32), fz, 32)
+        urec, xrec = O.sc_decode_recursive(mask, llr, fz)
+        assert np.array_equal(u64, u_naive) and np.array_equal(u32, u_naive)
+        assert np.array_equal(urec, u_naive)
+        assert np.array_equal(x64, O.polar_transform_bytes(u64)) and np.array_equal(x64, xrec)
+        assert np.allclose(st[3], leaf, rtol=1e-9, atol=1e-9)
+
+
+def test_sc_naive_awgn_n4():
+    rng = np.random.default_rng(5)
+    for _ in range(40):
+        mask = rng.integers(0, 2, 16).astype(np.uint8)
+        llr = rng.normal(1.0, 2.0, 16)
+        fz = rng.integers(0, 2, 16).astype(np.uint8)
+        u_naive, leaf = O.sc_decode_naive(mask, llr, fz)
+        u, _, st = O.sc_decode(mask, llr, fz, 64, dump=True)
+        assert np.array_equal(u, u_naive)
+        assert np.allclose(st[4], leaf, rtol=1e-9, atol=1e-9)
+
+
+@pytest.mark.parametrize("n", [6, 9, 12])
+def test_c_walk_matches_numpy_recursion(n):
+    rng = np.random.default_rng(n)
+    N = 1 << n
+    for fmode in (O.F_EXACT, O.F_MINSUM):
+        mask = (rng.random(N) < 0.5).astype(np.uint8)
+        llr = rng.normal(0.8, 1.5, N)
+        fz = rng.integers(0, 2, N).astype(np.uint8)
+        u, x = O.sc_decode(mask, llr, fz, 64, fmode=fmode)
+        ur, xr = O.sc_decode_recursive(mask, llr, fz, fmode=fmode)
+        assert np.array_equal(u, ur) and np.array_equal(x, xr)
+
+
+def test_noiseless_round_trip_n10():
+    """all-+-30 LLRs of x, consistent frozen values -> u exactly."""
+    rng = np.random.default_rng(3)
+    mask = (rng.random(1024) < 0.3).astype(np.uint8)
+    for _ in range(100):
+        x = rng.integers(0, 2, 1024).astype(np.uint8)
+        u = O.polar_transform_bytes(x)
+        llr = (1.0 - 2.0 * x) * 30.0
+        for prec in (64, 32):
+            uh, xh = O.sc_decode(mask, llr, u, prec)
+            assert np.array_equal(uh, u) and np.array_equal(xh, x)
+
+
+def test_batch_driver_matches_single():
+    rng = np.random.default_rng(9)
+    N = 256
+    mask = (rng.random(N) < 0.4).astype(np.uint8)
+    llr = rng.normal(1.0, 1.5, (6, N)).astype(np.float32)
+    fz = rng.integers(0, 2, (6, N)).astype(np.uint8)
+    for prec in (32, 64):
+        b = O.sc_decode_batch(mask, llr, fz, precision=prec, threads=3)
+        for f in range(6):
+            assert np.array_equal(b[f], O.sc_decode(mask, llr[f], fz[f], prec)[0])
+
+
+def test_de_oracle_acceptance6():
+    """Acceptance 6: reference DE pe at n=3 within 0.01 of genie-aided
+    enumeration over all 2^8 BSC outputs (uses the oracle's naive SC)."""
+    de = golden("de_small.npz")
+    for p in (0.05, 0.1):
+        c = np.log((1 - p) / p)
+        pe = np.zeros(8)
+        for pat in range(256):
+            e = ((pat >> np.arange(8)) & 1)
+            prob = np.prod(np.where(e == 1, p, 1 - p))
+            llr = (1 - 2 * e.astype(float)) * c  # all-zero codeword sent
+            # genie-aided: each bit-channel sees the true (zero) past
+            _, leaf = O.sc_decode_naive(np.ones(8, np.uint8), llr, np.zeros(8, np.uint8))
+            pe += prob * np.where(leaf < 0, 1.0, np.where(leaf == 0, 0.5, 0.0))
+        assert np.max(np.abs(pe - de[f"pe_{p}"])) < 0.01
