@@ -862,10 +862,10 @@ int pq_decoder_set_frozen_mask(pq_decoder *h, const uint8_t *mask)
 
 int pq_polar_transform(const uint32_t *in, uint32_t *out, int n, int frames, void *stream)
 {
-    if (!in || !out) return set_err(-1, "NULL pointer");
     if (n < 1 || n > 25) return set_err(-1, "n must be in [1, 25], got %d", n);
     if (frames < 0) return set_err(-1, "frames must be >= 0");
     if (frames == 0) return 0;
+    if (!in || !out) return set_err(-1, "NULL pointer");
     int launches = 0;
     return launch_transform(in, out, n, frames, nullptr, nullptr, (cudaStream_t)stream, &launches);
 }
@@ -952,6 +952,7 @@ static int decode_impl(pq_decoder *h, const float *llr, const uint32_t *ybits, f
 int pq_sc_decode_f32(pq_decoder *h, const float *llr, const uint32_t *frozen_u, uint32_t *u_hat,
                      uint32_t *x_hat, int frames, void *stream)
 {
+    if (frames == 0 && h) return 0;
     if (!llr) return set_err(-1, "llr is NULL");
     return decode_impl(h, llr, nullptr, 0.0f, frozen_u, u_hat, x_hat, nullptr, frames, stream);
 }
@@ -959,6 +960,7 @@ int pq_sc_decode_f32(pq_decoder *h, const float *llr, const uint32_t *frozen_u, 
 int pq_sc_decode_f32_dump(pq_decoder *h, const float *llr, const uint32_t *frozen_u, uint32_t *u_hat,
                           uint32_t *x_hat, float *dump, int frames, void *stream)
 {
+    if (frames == 0 && h) return 0;
     if (!llr || !dump) return set_err(-1, "llr/dump is NULL");
     return decode_impl(h, llr, nullptr, 0.0f, frozen_u, u_hat, x_hat, dump, frames, stream);
 }
@@ -966,6 +968,7 @@ int pq_sc_decode_f32_dump(pq_decoder *h, const float *llr, const uint32_t *froze
 int pq_sc_decode_bsc(pq_decoder *h, const uint32_t *y_bits, float llr_mag, const uint32_t *frozen_u,
                      uint32_t *u_hat, uint32_t *x_hat, int frames, void *stream)
 {
+    if (frames == 0 && h) return 0;
     if (!y_bits) return set_err(-1, "y_bits is NULL");
     if (!(llr_mag >= 0.0f)) return set_err(-1, "llr_mag must be >= 0");
     return decode_impl(h, nullptr, y_bits, llr_mag, frozen_u, u_hat, x_hat, nullptr, frames, stream);
