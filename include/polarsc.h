@@ -47,6 +47,10 @@ extern "C" {
                                  (decision-exact); 0: plain SC          */
 #define PQ_OPT_SUBTREE_LOG2 2 /* log2 of the shared-memory sub-tree width S; 0 = auto  */
 #define PQ_OPT_FMODE 3        /* PQ_F_EXACT / PQ_F_MINSUM                              */
+#define PQ_OPT_PROFILE 4      /* 1: record per-frame clock64 cycles per step class      */
+
+/* slots of the per-frame profile record (pq_decoder_read_profile) */
+#define PQ_PROF_SLOTS 16
 
 typedef struct pq_decoder pq_decoder;
 
@@ -100,6 +104,12 @@ int pq_sc_decode_bsc(pq_decoder *h, const uint32_t *y_bits, float llr_mag,
  * in and out may alias.  Replaces: polar_transform(u),
  * also alice_disclose's u = polar_transform(x).             */
 int pq_polar_transform(const uint32_t *in, uint32_t *out, int n, int frames, void *stream);
+
+/* Copy the per-frame cycle profile of the last decode (PQ_OPT_PROFILE=1):
+ * out[frame][PQ_PROF_SLOTS] = {upper f, upper g, upper other, shared f,
+ * shared g, shared other, warp sub-trees, type staging, rate-1, total,
+ * #warp sub-trees, #block nodes, ...}.  Synchronous.  Diagnostics only. */
+int pq_decoder_read_profile(const pq_decoder *h, unsigned long long *out, int frames);
 
 /* Bytes of device scratch owned by the handle. */
 size_t pq_decoder_workspace_bytes(const pq_decoder *h);

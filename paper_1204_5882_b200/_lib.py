@@ -17,13 +17,17 @@ PQ_F_MINSUM = 1
 PQ_OPT_SSC = 1
 PQ_OPT_SUBTREE_LOG2 = 2
 PQ_OPT_FMODE = 3
+PQ_OPT_PROFILE = 4
+PQ_PROF_SLOTS = 16
+PROF_NAMES = ("upper_f", "upper_g", "upper_other", "smem_f", "smem_g", "smem_other", "warp_subtrees",
+              "type_staging", "rate1_block", "total", "n_warp_subtrees", "n_block_nodes")
 
 # every symbol include/polarsc.h declares (tests check the .so exports them)
 EXPORTS = (
     "pq_decoder_create", "pq_decoder_set_frozen_mask", "pq_decoder_set_option",
     "pq_decoder_get_option", "pq_sc_decode_f32", "pq_sc_decode_f32_dump", "pq_sc_decode_bsc",
     "pq_polar_transform", "pq_decoder_workspace_bytes", "pq_decoder_last_launches",
-    "pq_decoder_destroy", "pq_last_error", "pq_abi_version",
+    "pq_decoder_destroy", "pq_last_error", "pq_abi_version", "pq_decoder_read_profile",
 )
 
 _lib = None
@@ -56,6 +60,7 @@ def load():
     L.pq_decoder_workspace_bytes.restype = ctypes.c_size_t
     L.pq_decoder_last_launches.argtypes = [vp]
     L.pq_decoder_destroy.argtypes = [vp]
+    L.pq_decoder_read_profile.argtypes = [vp, vp, i]
     L.pq_last_error.restype = ctypes.c_char_p
     L.pq_abi_version.restype = ctypes.c_int
     for name in EXPORTS:

@@ -191,7 +191,12 @@ struct DecParams {
     float *scr;                  // [F][N] stage buffers for widths > S
     uint32_t *X;                 // [F][wpf] out: shifted x-hat partial sums
     float *dump;                 // [F][n+1][N] stage dump (plain mode), or null
+    unsigned long long *prof;    // [F][PQ_PROF_SLOTS] clock64 cycles per step class, or null
 };
+
+// step classes for the optional per-frame cycle profile (PQ_OPT_PROFILE)
+enum { PR_UP_F = 0, PR_UP_G, PR_UP_OTHER, PR_SM_F, PR_SM_G, PR_SM_OTHER, PR_WARP, PR_TYPES, PR_RATE1,
+       PR_TOTAL, PR_NODES_WARP, PR_NODES_BLOCK };
 
 struct FrameCtx {
     const float *llr;
@@ -429,18 +434,39 @@ __global__ void __launch_bounds__(256) sc_decode_kernel(DecParams p)
     int d = 0;
     uint32_t j = 0;
     bool entering = true;
+    // profile: thread 0 charges the cycles since the previous mark to the class
+    // of the step that just ran (every step starts behind a barrier)
+    unsigned long long pr_acc[PQ_PROF_SLOTS];
+    unsigned long long pr_last = 0, pr_start = 0;
+    int pr_cls = PR_SM_OTHER;
+    const bool prof = p.prof != nullptr && tid == 0;
+    if (prof) {
+        for (int q = 0; q < PQ_PROF_SLOTS; q++) pr_acc[q] = 0;
+        pr_start = pr_last = clock64();
+    }
+#define PROF_MARK(cls)                                         \
+    do {                                                       \
+        if (prof) {                                            \
+            const unsigned long long now_ = clock64();         \
+            pr_acc[pr_cls] += now_ - pr_last;                  \
+            pr_last = now_;                                    \
+            pr_cls = (cls);                                    \
+        }                                                      \
+    } while (0)
     for (;;) {
         const uint32_t W = N >> d;
         if (entering) {
             uint8_t t = ntype(d, j);
             if (p.plain && W > 1) t = NT_MIXED;
             if (t == NT_RATE0) {
+                PROF_MARK(W > S ? PR_UP_OTHER : PR_SM_OTHER);
                 __syncthreads();
                 zero_bits_block(xptr(W), xpos(W, j * W), W);
                 entering = false;
                 continue;
             }
             if (W == S) {
+                PROF_MARK(PR_TYPES);
                 // entering a shared-memory sub-tree: stage its node types
                 __syncthreads();
                 for (uint32_t q = 1 + tid; q < 2 * S; q += nthr) {
@@ -449,6 +475,8 @@ __global__ void __launch_bounds__(256) sc_decode_kernel(DecParams p)
                 }
             }
             if (W <= 64) {
+                PROF_MARK(PR_WARP);
+                if (prof) pr_acc[PR_NODES_WARP]++;
                 __syncthreads();
                 if (tid < 32) {
                     const bool chan = d == 0;
@@ -472,6 +500,7 @@ __global__ void __launch_bounds__(256) sc_decode_kernel(DecParams p)
             }
             const float *src = d == 0 ? nullptr : stage_ptr(p, fc, sm, W);
             if (t == NT_RATE1 && !p.plain) {
+                PROF_MARK(PR_RATE1);
                 __syncthreads();
                 float m = __int_as_float(0x7f800000);
                 for (uint32_t i = tid; i < W; i += nthr) {
@@ -497,6 +526,8 @@ __global__ void __launch_bounds__(256) sc_decode_kernel(DecParams p)
             // mixed node: f-step into the left child unless it is rate-0
             const uint32_t H = W / 2;
             const uint8_t tl = p.plain ? NT_MIXED : ntype(d + 1, 2 * j);
+            PROF_MARK(W > S ? PR_UP_F : PR_SM_F);
+            if (prof) pr_acc[PR_NODES_BLOCK]++;
             __syncthreads();
             if (tl == NT_RATE0) {
                 zero_bits_block(xptr(H), xpos(H, 2 * j * H), H);
@@ -520,6 +551,7 @@ __global__ void __launch_bounds__(256) sc_decode_kernel(DecParams p)
         }
         // ---- node (d, j) is decided; its partial sums are in place
         if (W == S && S < N) {
+            PROF_MARK(PR_UP_OTHER);
             __syncthreads();
             for (uint32_t w = tid; w < S / 32; w += nthr) fc.X[(j * S) / 32 + w] = sm.xs[w];
         }
@@ -532,12 +564,18 @@ __global__ void __launch_bounds__(256) sc_decode_kernel(DecParams p)
                     fc.X[0] = sm.xs[0] & ((1u << N) - 1u);
                 }
             }
+            PROF_MARK(PR_SM_OTHER);
+            if (prof) {
+                pr_acc[PR_TOTAL] = clock64() - pr_start;
+                for (int q = 0; q < PQ_PROF_SLOTS; q++) p.prof[(size_t)frame * PQ_PROF_SLOTS + q] = pr_acc[q];
+            }
             break;
         }
         if ((j & 1) == 0) {
             // left child done -> g-step at the parent into the right child
             const uint32_t jr = j + 1;
             const uint8_t tr = p.plain ? NT_MIXED : ntype(d, jr);
+            PROF_MARK(2 * W > S ? PR_UP_G : PR_SM_G);
             __syncthreads();
             if (tr == NT_RATE0) {
                 zero_bits_block(xptr(W), xpos(W, jr * W), W);
@@ -562,6 +600,7 @@ __global__ void __launch_bounds__(256) sc_decode_kernel(DecParams p)
             continue;
         }
         // right child done -> parent's partial sums = (xl ^ xr, xr)
+        PROF_MARK(2 * W > S ? PR_UP_OTHER : PR_SM_OTHER);
         __syncthreads();
         combine_block(xptr(2 * W), xpos(2 * W, (j - 1) * W), W);
         d--;
@@ -703,6 +742,8 @@ struct pq_decoder {
     size_t scr_elems;
     size_t ws_bytes;
     int last_launches;
+    int profile;
+    unsigned long long *d_prof;
 };
 
 static int choose_log2S(const pq_decoder *h, int frames)
@@ -789,6 +830,7 @@ int pq_decoder_destroy(pq_decoder *h)
     cudaFree(h->d_cw);
     cudaFree(h->d_x);
     cudaFree(h->d_scr);
+    cudaFree(h->d_prof);
     delete h;
     return 0;
 }
@@ -809,8 +851,25 @@ int pq_decoder_set_option(pq_decoder *h, int key, int value)
         if (value != PQ_F_EXACT && value != PQ_F_MINSUM) return set_err(-1, "unknown f mode %d", value);
         h->fmode = value;
         return 0;
+    case PQ_OPT_PROFILE:
+        if (value && !h->d_prof) {
+            cudaError_t e = cudaMalloc((void **)&h->d_prof, (size_t)h->max_frames * PQ_PROF_SLOTS * 8);
+            if (e != cudaSuccess) return set_err(1 + (int)e, "cudaMalloc(profile): %s", cudaGetErrorString(e));
+            cudaMemset(h->d_prof, 0, (size_t)h->max_frames * PQ_PROF_SLOTS * 8);
+        }
+        h->profile = value ? 1 : 0;
+        return 0;
     default: return set_err(-1, "unknown option %d", key);
     }
+}
+
+int pq_decoder_read_profile(const pq_decoder *h, unsigned long long *out, int frames)
+{
+    if (!h || !out) return set_err(-1, "NULL argument");
+    if (!h->d_prof) return set_err(-1, "profiling was never enabled (PQ_OPT_PROFILE)");
+    if (frames < 0 || frames > h->max_frames) return set_err(-1, "bad frame count");
+    CUDA_TRY(cudaMemcpy(out, h->d_prof, (size_t)frames * PQ_PROF_SLOTS * 8, cudaMemcpyDeviceToHost));
+    return 0;
 }
 
 int pq_decoder_get_option(const pq_decoder *h, int key)
@@ -820,6 +879,7 @@ int pq_decoder_get_option(const pq_decoder *h, int key)
     case PQ_OPT_SSC: return h->ssc;
     case PQ_OPT_SUBTREE_LOG2: return h->log2S_opt;
     case PQ_OPT_FMODE: return h->fmode;
+    case PQ_OPT_PROFILE: return h->profile;
     default: return set_err(-1, "unknown option %d", key);
     }
 }
@@ -906,6 +966,7 @@ static int decode_impl(pq_decoder *h, const float *llr, const uint32_t *ybits, f
     p.scr = h->d_scr;
     p.X = h->d_x;
     p.dump = dump;
+    p.prof = h->profile ? h->d_prof : nullptr;
     const size_t smem = dec_smem_bytes(p.S);
     if (h->fmode == PQ_F_MINSUM) {
         CUDA_TRY(cudaFuncSetAttribute(sc_decode_kernel<PQ_F_MINSUM>, cudaFuncAttributeMaxDynamicSharedMemorySize,

@@ -139,6 +139,14 @@ class ScDecoder:
     def last_launches(self) -> int:
         return int(_lib.load().pq_decoder_last_launches(self._h))
 
+    def read_profile(self, frames: int) -> np.ndarray:
+        """[frames, PQ_PROF_SLOTS] clock64 cycles per step class of the last
+        decode (set_option(PQ_OPT_PROFILE, 1) first)."""
+        out = np.zeros((frames, _lib.PQ_PROF_SLOTS), np.uint64)
+        _lib.check(_lib.load().pq_decoder_read_profile(self._h, out.ctypes.data, frames),
+                   "pq_decoder_read_profile")
+        return out
+
     def alloc_words(self, frames: int):
         return torch.empty((frames, self.wpf), dtype=torch.int32, device=self.device)
 
