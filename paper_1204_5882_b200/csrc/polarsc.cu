@@ -70,17 +70,40 @@ static int set_err(int code, const char *fmt, ...)
     } while (0)
 
 // ---------------------------------------------------------------------------
-// device math: the exact boxplus in IEEE-only fp32 (mirrored by
-// oracle/sc_oracle.c:orc_fmag_f32; the two must agree bit for bit)
+// device math: the exact boxplus in branch-free, IEEE-only fp32 (add, mul,
+// fma, rint and integer bit operations -- no MUFU, no division).  Mirrored
+// operation for operation by oracle/sc_oracle.c:orc_fmag_f32; the two must
+// agree bit for bit (tests/test_gpu_parity.py checks every stage LLR).
 
 #define LN2_HI 0.693145751953125f
 #define LN2_LO 1.42860682030941723212e-6f
 #define INV_LN2 1.44269504088896341f
 
-// e = e^-x, m = 1 - e^-x for x >= 0: Cody-Waite reduction, Taylor-7 expm1
+// 1/T_j and log(T_j), T_j = 1 + j/32, rounded to fp32 (same bits in the oracle)
+__constant__ uint32_t c_log_tab[64] = {
+    0x3f800000u, 0x3f783e10u, 0x3f70f0f1u, 0x3f6a0ea1u, 0x3f638e39u, 0x3f5d67c9u, 0x3f579436u, 0x3f520d21u,
+    0x3f4ccccdu, 0x3f47ce0cu, 0x3f430c31u, 0x3f3e82fau, 0x3f3a2e8cu, 0x3f360b61u, 0x3f321643u, 0x3f2e4c41u,
+    0x3f2aaaabu, 0x3f272f05u, 0x3f23d70au, 0x3f20a0a1u, 0x3f1d89d9u, 0x3f1a90e8u, 0x3f17b426u, 0x3f14f209u,
+    0x3f124925u, 0x3f0fb824u, 0x3f0d3dcbu, 0x3f0ad8f3u, 0x3f088889u, 0x3f064b8au, 0x3f042108u, 0x3f020821u,
+    0x00000000u, 0x3cfc14d8u, 0x3d785186u, 0x3db78694u, 0x3df1383bu, 0x3e14aa98u, 0x3e2ff984u, 0x3e4a92d5u,
+    0x3e647fbeu, 0x3e7dc8c3u, 0x3e8b3ae5u, 0x3e974716u, 0x3ea30c5eu, 0x3eae8deeu, 0x3eb9cec0u, 0x3ec4d19cu,
+    0x3ecf991fu, 0x3eda27bcu, 0x3ee47fbeu, 0x3eeea350u, 0x3ef8947bu, 0x3f012a95u, 0x3f05f397u, 0x3f0aa61fu,
+    0x3f0f42fbu, 0x3f13caf1u, 0x3f183ebau, 0x3f1c9f07u, 0x3f20ec7fu, 0x3f2527c3u, 0x3f295169u, 0x3f2d6a02u};
+// staged into shared memory at kernel start: lanes index it with divergent j,
+// which shared memory serves without bank conflicts (32 distinct words)
+__shared__ float pq_tab[64];
+
+__device__ __forceinline__ void load_log_table()
+{
+    for (int i = threadIdx.x; i < 64; i += blockDim.x) pq_tab[i] = __uint_as_float(c_log_tab[i]);
+}
+
+// e = e^-x, m = 1 - e^-x for x >= 0 (x clamped at 86.5: e stays a normal
+// float; beyond that e^-x < 2.3e-38 never changes a result).
+// Cody-Waite reduction x = k ln2 + r, |r| <= ln2/2; Taylor-7 expm1(-r).
 __device__ __forceinline__ void pq_expm(float x, float &e, float &m)
 {
-    x = x > 100.0f ? 100.0f : x;
+    x = fminf(x, 86.5f);
     const float kf = rintf(x * INV_LN2);
     float r = fmaf(-kf, LN2_HI, x);
     r = fmaf(-kf, LN2_LO, r);
@@ -92,63 +115,64 @@ __device__ __forceinline__ void pq_expm(float x, float &e, float &m)
     h = fmaf(t, h, 1.0f / 6.0f);
     h = fmaf(t, h, 0.5f);
     const float p = fmaf(t * t, h, t);
-    const int k = (int)kf;
-    if (k > 125) {
-        e = 0.0f;
-        m = 1.0f;
-    } else {
-        const float s = __uint_as_float((uint32_t)(127 - k) << 23);
-        e = fmaf(s, p, s);
-        m = fmaf(-s, p, 1.0f - s);
-    }
+    const float s = __uint_as_float((uint32_t)(127 - (int)kf) << 23);  // 2^-k
+    e = fmaf(s, p, s);
+    m = fmaf(-s, p, 1.0f - s);
 }
 
-// log1p(num / den), den > 0, num/den >= -0.5
-__device__ __forceinline__ float pq_log1p_ratio(float num, float den)
+// 1/d for d in [2^-126, 2]: integer seed, three Newton steps (FMA only)
+__device__ __forceinline__ float pq_rcp(float d)
 {
-    float s, kf;
-    if (num >= -0.29289322f * den && num <= 0.41421356f * den) {
-        s = num / (2.0f * den + num);
-        kf = 0.0f;
-    } else {
-        const float u = 1.0f + num / den;
-        const uint32_t b = __float_as_uint(u);
-        int k = (int)((b >> 23) & 0xffu) - 127;
-        float mm = __uint_as_float((b & 0x007fffffu) | 0x3f800000u);
-        if (mm > 1.41421356f) {
-            mm *= 0.5f;
-            k += 1;
-        }
-        s = (mm - 1.0f) / (mm + 1.0f);
-        kf = (float)k;
-    }
-    const float z = s * s;
-    float h = fmaf(z, 1.0f / 11.0f, 1.0f / 9.0f);
-    h = fmaf(z, h, 1.0f / 7.0f);
-    h = fmaf(z, h, 1.0f / 5.0f);
-    h = fmaf(z, h, 1.0f / 3.0f);
-    const float s2 = s + s;
-    const float p = fmaf(s2 * z, h, s2);
-    return fmaf(kf, LN2_HI, fmaf(kf, LN2_LO, p));
+    float r = __uint_as_float(0x7ef311c7u - __float_as_uint(d));
+    float e = fmaf(-d, r, 1.0f);
+    r = fmaf(r, e, r);
+    e = fmaf(-d, r, 1.0f);
+    r = fmaf(r, e, r);
+    e = fmaf(-d, r, 1.0f);
+    return fmaf(r, e, r);
 }
 
-// |f| for magnitudes a, b >= 0:
-//   log1p((1-e^-lo)(1-e^-hi) / (e^-lo + e^-hi))     lo <= 40
-//   lo + log1p(-e / (1 + e)), e = e^-(hi-lo)        lo >  40
+// log1p(q), 0 <= q < 2^100: u = 1 + q with its exact rounding error (Fast2Sum),
+// u = 2^k m, m in [T_j, T_j + 1/32), log m = log T_j + log1p((m - T_j)/T_j)
+__device__ __forceinline__ float pq_log1p(float q)
+{
+    const float u = 1.0f + q;
+    const float err = (fmaxf(1.0f, q) - u) + fminf(1.0f, q);
+    const uint32_t b = __float_as_uint(u);
+    const int k = (int)(b >> 23) - 127;
+    const uint32_t j = (b >> 18) & 31u;
+    const float m = __uint_as_float((b & 0x007fffffu) | 0x3f800000u);
+    const float T = __uint_as_float(0x3f800000u | (j << 18));
+    const float invT = pq_tab[j], logT = pq_tab[32 + j];
+    const float r = (m - T) * invT;
+    float p = fmaf(r, -1.0f / 6.0f, 0.2f);
+    p = fmaf(r, p, -0.25f);
+    p = fmaf(r, p, 1.0f / 3.0f);
+    p = fmaf(r, p, -0.5f);
+    p = fmaf(r, p, 1.0f);
+    p = p * r;
+    const float inv_u = __uint_as_float((uint32_t)(127 - k) << 23) * invT;
+    const float kf = (float)k;
+    return fmaf(kf, LN2_HI, fmaf(kf, LN2_LO, logT + (p + err * inv_u)));
+}
+
+// |f| for magnitudes a, b >= 0 (lo = min, hi = max):
+//   lo <= 8:  log1p((1 - e^-lo)(1 - e^-hi) / (e^-lo + e^-hi))
+//   lo >  8:  lo - log1p(e^-(hi - lo))      (drops log1p(e^-(lo+hi)) < 1.2e-7, i.e.
+//                                            < 2e-8 relative to a result >= 7.3)
 // = log((1 + e^-a e^-b)/(e^-a + e^-b)) = phi(phi(a) + phi(b)),
-// the reference's stable boxplus (construction.py:300-303) without its
-// small-magnitude cancellation.
+// the reference's stable boxplus (construction.py:300-303) in a form free of
+// its cancellation at small magnitudes.  Max relative error ~3.4e-7.
 __device__ __forceinline__ float pq_fmag(float a, float b)
 {
     const float lo = fminf(a, b), hi = fmaxf(a, b);
-    const bool big = lo > 40.0f;
+    const bool big = lo > 8.0f;
     float e1, m1, e2, m2;
     pq_expm(big ? hi - lo : lo, e1, m1);
     pq_expm(hi, e2, m2);
-    const float num = big ? -e1 : m1 * m2;
-    const float den = big ? 1.0f + e1 : e1 + e2;
-    const float base = big ? lo : 0.0f;
-    return base + pq_log1p_ratio(num, den);
+    const float q = (m1 * m2) * pq_rcp(e1 + e2);
+    const float l = pq_log1p(big ? e1 : q);
+    return big ? lo - l : l;
 }
 
 template <int FM>
@@ -394,6 +418,8 @@ __global__ void __launch_bounds__(256) sc_decode_kernel(DecParams p)
     const uint32_t SW = S >= 32 ? S / 32 : 1;
     sm.ty = (uint8_t *)(sm.xs + SW);
 
+    load_log_table();
+    __syncthreads();
     const uint32_t frame = blockIdx.x;
     FrameCtx fc;
     fc.llr = p.llr ? p.llr + (size_t)frame * N : nullptr;
