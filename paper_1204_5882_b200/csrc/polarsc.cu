@@ -256,76 +256,241 @@ __device__ __forceinline__ float *stage_ptr(const DecParams &p, const FrameCtx &
 }
 
 // ---------------------------------------------------------------------------
-// warp-level sub-tree decoder, W <= 64, LLRs in registers:
-// W <= 32: lane l holds element l in v0;  W == 64: v0 = element l, v1 = element l+32.
-// Returns the node's W partial-sum bits (uniform across the warp).
+// warp-level decoding of sub-trees of width W <= 256, all LLRs in registers.
+//
+// W = 32V (V = 2, 4, 8): lane l holds elements l + 32t, t < V.  The f- and
+// g-steps down to W = 32 are in-lane (element i pairs with i + W/2 in the
+// same lane), so these levels need no shuffles at all.
+//
+// W <= 32: an iterative engine (no calls, no local memory).  Register A holds
+// the root node (lane l = element l); register B holds the current node of
+// every depth e >= 1 side by side, depth e at lanes [o(e), o(e) + 32>>e) with
+// o(e) = 32 - 2^(6-e) (0, 16, 24, 28, 30).  The f-step stores the shuffled
+// operand pair (a, b) in registers Ca/Cb at the child's lanes, so the later
+// g-step of the same node reuses them without shuffling.  Left-child partial
+// sums of every depth are packed into one uniform word XL at bit offset o(e).
+// Node types (2 bits each) and the leaf frozen bits are fetched once per
+// engine entry into three uniform bit masks.
+
+__device__ __forceinline__ int eng_off(int e) { return e == 0 ? 0 : 32 - (64 >> e); }
+__device__ __forceinline__ uint32_t lowmask(int w) { return w >= 32 ? 0xffffffffu : ((1u << w) - 1u); }
+__device__ __forceinline__ int ilog2(uint32_t w) { return 31 - __clz(w); }
 
 struct WarpCtx {
-    const uint8_t *ty;   // local heap types of the current S-sub-tree (smem)
-    float *dump;         // frame dump base or null
+    const uint8_t *ty;   // S-sub-tree-local heap types (shared memory)
+    float *dump;         // frame dump base (plain mode) or null
     uint32_t N;
     int plain;
+    int dS;              // absolute depth of the S-sub-tree root
+    uint32_t jS;         // its index
 };
 
-template <int W, int FM>
-__device__ __noinline__ uint64_t wdec(float v0, float v1, int lh, const WarpCtx &c, int d, uint32_t j)
+// Decode the node at S-local heap index `root` (width W0 <= 32, A holds its
+// values: lane l = element l for l < W0).  Returns its W0 partial-sum bits.
+template <int FM>
+__device__ __forceinline__ uint32_t engine32(float A, uint32_t root, int W0, const WarpCtx &c)
 {
+    const unsigned FULL = 0xffffffffu;
     const int lane = threadIdx.x & 31;
-    const uint8_t t = c.ty[lh];
-    if (t == NT_RATE0 && (W == 1 || !c.plain)) return 0;
-    if constexpr (W == 1) {
-        const float L = __shfl_sync(0xffffffffu, v0, 0);
-        return L < 0.0f ? 1ull : 0ull;
+    const int e0 = 5 - ilog2((uint32_t)W0);
+    // fetch the sub-tree's node types: lane h (1 <= h < W0) internal node h,
+    // lane h (< W0) also the leaf W0 + h
+    uint32_t tint = NT_MIXED, tleaf = NT_RATE1;
+    {
+        const int eh = lane >= 1 ? ilog2((uint32_t)lane) : 0;
+        if (lane >= 1 && lane < W0) tint = c.ty[(root << eh) + (uint32_t)(lane - (1 << eh))];
+        const int el = ilog2((uint32_t)W0);
+        if (lane < W0) tleaf = c.ty[(root << el) + (uint32_t)lane];
+    }
+    if (c.plain) tint = NT_MIXED;
+    const uint32_t tb0 = __ballot_sync(FULL, tint & 1u), tb1 = __ballot_sync(FULL, tint & 2u);
+    const uint32_t leaf0 = __ballot_sync(FULL, tleaf == NT_RATE0);
+    auto ntype = [&](int h) -> uint32_t { return ((tb0 >> h) & 1u) | (((tb1 >> h) & 1u) << 1); };
+    // absolute node coordinates for the stage dump
+    const int el0 = ilog2(root);
+    const int d_root = c.dS + el0;
+    const uint32_t j_root = (c.jS << el0) + (root - (1u << el0));
+
+    float B = A, Ca = 0.0f, Cb = 0.0f;
+    if (e0 > 0) B = __shfl_sync(FULL, A, (lane - eng_off(e0)) & 31);
+    int e = e0;
+    uint32_t j = 0, xnode = 0, XL = 0;
+    bool entering = true;
+    for (;;) {
+        const int w = 32 >> e;
+        const int o = eng_off(e);
+        const float P = e == 0 ? A : B;
+        const int h = (1 << (e - e0)) + (int)j;  // engine-local heap index
+        if (entering) {
+            if (w == 1) {
+                const float L = __shfl_sync(FULL, P, o);
+                xnode = ((leaf0 >> j) & 1u) ? 0u : (L < 0.0f ? 1u : 0u);
+                entering = false;
+                continue;
+            }
+            const uint32_t t = ntype(h);
+            const bool in = lane >= o && lane < o + w;
+            if (t == NT_RATE0) {
+                xnode = 0;
+                entering = false;
+                continue;
+            }
+            if (t == NT_RATE1) {
+                uint32_t m = in ? (__float_as_uint(P) & 0x7fffffffu) : 0x7f800000u;
+                m = __reduce_min_sync(FULL, m);
+                if (rate1_guard(__uint_as_float(m), ilog2((uint32_t)w))) {
+                    xnode = (__ballot_sync(FULL, in && P < 0.0f) >> o) & lowmask(w);
+                    entering = false;
+                    continue;
+                }
+            }
+            if (t == NT_REP) {
+                // last-leaf LLR = SC's g-chain with zero partial sums, in SC's own
+                // pairing order: r_i = L[i + w/2] + L[i], halving down to one value
+                float sum = P;
+                for (int hh = w / 2; hh >= 1; hh >>= 1) {
+                    const float other = __shfl_down_sync(FULL, sum, hh);
+                    sum = other + sum;
+                }
+                const float L = __shfl_sync(FULL, sum, o);
+                xnode = L < 0.0f ? lowmask(w) : 0u;
+                entering = false;
+                continue;
+            }
+            // mixed: f-step into the left child (operands kept in Ca/Cb)
+            const int oc = eng_off(e + 1), hw = w / 2;
+            const int src = o + (lane - oc);
+            const float a = __shfl_sync(FULL, P, src & 31);
+            const float b = __shfl_sync(FULL, P, (src + hw) & 31);
+            const bool inc = lane >= oc && lane < oc + hw;
+            Ca = inc ? a : Ca;
+            Cb = inc ? b : Cb;
+            const bool lft0 = hw == 1 ? ((leaf0 >> (2 * j)) & 1u) != 0 : ntype(2 * h) == NT_RATE0;
+            if (lft0 && !c.plain) {
+                XL &= ~(lowmask(hw) << oc);  // left child decided: all zero
+                e++;
+                j = 2 * j;
+                xnode = 0;
+                entering = false;
+                continue;
+            }
+            const float fv = pq_f<FM>(a, b);
+            B = inc ? fv : B;
+            if (c.dump && inc)
+                c.dump[(size_t)(d_root + e - e0 + 1) * c.N + ((size_t)j_root << (e - e0 + 1)) * hw +
+                       (size_t)(2 * j) * hw + (lane - oc)] = fv;
+            e++;
+            j = 2 * j;
+            continue;
+        }
+        // node (e, j) is decided with partial sums xnode
+        if (e == e0) return xnode;
+        if ((j & 1u) == 0) {
+            XL = (XL & ~(lowmask(w) << o)) | (xnode << o);
+            const bool rgt0 = w == 1 ? ((leaf0 >> (j + 1)) & 1u) != 0 : ntype(h + 1) == NT_RATE0;
+            j++;
+            if (rgt0 && !c.plain) {
+                xnode = 0;
+                continue;  // right child decided too
+            }
+            const bool inc = lane >= o && lane < o + w;
+            const uint32_t sbit = (xnode >> ((lane - o) & 31)) & 1u;
+            const float gv = pq_g(Ca, Cb, sbit);
+            B = inc ? gv : B;
+            if (c.dump && inc)
+                c.dump[(size_t)(d_root + e - e0) * c.N + ((size_t)j_root << (e - e0)) * w + (size_t)j * w +
+                       (lane - o)] = gv;
+            entering = true;
+            continue;
+        }
+        const uint32_t xl = (XL >> o) & lowmask(w);
+        xnode = (xl ^ xnode) | (xnode << w);
+        e--;
+        j >>= 1;
+    }
+}
+
+// W = 32V node at S-local heap index lh; v[t] = element lane + 32t.
+// out[t] = partial-sum word t (bits of elements 32t .. 32t+31).
+template <int FM, int V>
+__device__ __forceinline__ void wlevel(const float (&v)[V], uint32_t lh, const WarpCtx &c, uint32_t (&out)[V])
+{
+    const unsigned FULL = 0xffffffffu;
+    const int lane = threadIdx.x & 31;
+    uint8_t t = c.ty[lh];
+    if (c.plain) t = NT_MIXED;
+    if (t == NT_RATE0) {
+#pragma unroll
+        for (int q = 0; q < V; q++) out[q] = 0;
+        return;
+    }
+    if (t == NT_RATE1) {
+        uint32_t m = 0x7f800000u;
+#pragma unroll
+        for (int q = 0; q < V; q++) m = min(m, __float_as_uint(v[q]) & 0x7fffffffu);
+        m = __reduce_min_sync(FULL, m);
+        if (rate1_guard(__uint_as_float(m), 5 + ilog2((uint32_t)V))) {
+#pragma unroll
+            for (int q = 0; q < V; q++) out[q] = __ballot_sync(FULL, v[q] < 0.0f);
+            return;
+        }
+    }
+    if (t == NT_REP) {
+        float sum[V];
+#pragma unroll
+        for (int q = 0; q < V; q++) sum[q] = v[q];
+#pragma unroll
+        for (int hv = V / 2; hv >= 1; hv >>= 1)
+#pragma unroll
+            for (int q = 0; q < hv; q++) sum[q] = sum[q + hv] + sum[q];
+        float s0 = sum[0];
+        for (int hh = 16; hh >= 1; hh >>= 1) {
+            const float other = __shfl_down_sync(FULL, s0, hh);
+            s0 = other + s0;
+        }
+        const float L = __shfl_sync(FULL, s0, 0);
+#pragma unroll
+        for (int q = 0; q < V; q++) out[q] = L < 0.0f ? FULL : 0u;
+        return;
+    }
+    constexpr int H = V / 2;
+    const int el = ilog2(lh);
+    const int d = c.dS + el;
+    const uint32_t j = (c.jS << el) + (lh - (1u << el));
+    const uint32_t Wc = 32u * H;  // child width
+    float ch[H];
+    uint32_t xl[H], xr[H];
+    const bool skipl = !c.plain && c.ty[2 * lh] == NT_RATE0;
+    if (skipl) {
+#pragma unroll
+        for (int q = 0; q < H; q++) xl[q] = 0;
     } else {
-        constexpr int H = W / 2;
-        constexpr uint64_t FULLW = W == 64 ? ~0ull : ((1ull << W) - 1);
-        if (!c.plain && t == NT_RATE1) {
-            uint32_t m = lane < W ? (__float_as_uint(v0) & 0x7fffffffu) : 0x7f800000u;
-            if (W == 64) m = min(m, __float_as_uint(v1) & 0x7fffffffu);
-            m = __reduce_min_sync(0xffffffffu, m);
-            int k = 0;
-            for (int w = W; w > 1; w >>= 1) k++;
-            if (rate1_guard(__uint_as_float(m), k)) {
-                uint64_t bits = __ballot_sync(0xffffffffu, v0 < 0.0f);
-                if (W == 64) bits |= (uint64_t)__ballot_sync(0xffffffffu, v1 < 0.0f) << 32;
-                return bits & FULLW;
-            }
-        }
-        if (!c.plain && t == NT_REP) {
-            // last-leaf LLR of a repetition node = SC's g-chain with zero partial
-            // sums, summed in SC's own pairing order (r_i = L[i+w/2] + L[i])
-            float s = W == 64 ? v1 + v0 : v0;
-            for (int h = (W == 64 ? 16 : H); h >= 1; h >>= 1) {
-                const float o = __shfl_down_sync(0xffffffffu, s, h);
-                s = o + s;
-            }
-            const float L = __shfl_sync(0xffffffffu, s, 0);
-            return L < 0.0f ? FULLW : 0ull;
-        }
-        float a, b;
-        if (W == 64) {
-            a = v0;
-            b = v1;
-        } else {
-            a = v0;
-            b = __shfl_down_sync(0xffffffffu, v0, H);
-        }
-        uint64_t xl = 0;
-        const bool skipl = !c.plain && c.ty[2 * lh] == NT_RATE0;
-        if (!skipl) {
-            const float fl = pq_f<FM>(a, b);
-            if (c.dump && lane < H) c.dump[(size_t)(d + 1) * c.N + (size_t)(2 * j) * H + lane] = fl;
-            xl = wdec<H, FM>(fl, 0.0f, 2 * lh, c, d + 1, 2 * j);
-        }
-        uint64_t xr = 0;
-        const bool skipr = !c.plain && c.ty[2 * lh + 1] == NT_RATE0;
-        if (!skipr) {
-            const uint32_t s = (uint32_t)(xl >> lane) & 1u;
-            const float gr = pq_g(a, b, s);
-            if (c.dump && lane < H) c.dump[(size_t)(d + 1) * c.N + (size_t)(2 * j + 1) * H + lane] = gr;
-            xr = wdec<H, FM>(gr, 0.0f, 2 * lh + 1, c, d + 1, 2 * j + 1);
-        }
-        return (xl ^ xr) | (xr << H);
+#pragma unroll
+        for (int q = 0; q < H; q++) ch[q] = pq_f<FM>(v[q], v[q + H]);
+        if (c.dump)
+#pragma unroll
+            for (int q = 0; q < H; q++) c.dump[(size_t)(d + 1) * c.N + (size_t)(2 * j) * Wc + 32 * q + lane] = ch[q];
+        if constexpr (H == 1) xl[0] = engine32<FM>(ch[0], 2 * lh, 32, c);
+        else wlevel<FM, H>(ch, 2 * lh, c, xl);
+    }
+    const bool skipr = !c.plain && c.ty[2 * lh + 1] == NT_RATE0;
+    if (skipr) {
+#pragma unroll
+        for (int q = 0; q < H; q++) xr[q] = 0;
+    } else {
+#pragma unroll
+        for (int q = 0; q < H; q++) ch[q] = pq_g(v[q], v[q + H], (xl[q] >> lane) & 1u);
+        if (c.dump)
+#pragma unroll
+            for (int q = 0; q < H; q++)
+                c.dump[(size_t)(d + 1) * c.N + (size_t)(2 * j + 1) * Wc + 32 * q + lane] = ch[q];
+        if constexpr (H == 1) xr[0] = engine32<FM>(ch[0], 2 * lh + 1, 32, c);
+        else wlevel<FM, H>(ch, 2 * lh + 1, c, xr);
+    }
+#pragma unroll
+    for (int q = 0; q < H; q++) {
+        out[q] = xl[q] ^ xr[q];
+        out[H + q] = xr[q];
     }
 }
 
@@ -389,25 +554,44 @@ __device__ __forceinline__ float block_min(float v, float *red)
 // ---------------------------------------------------------------------------
 // the per-frame tree walk
 
-template <int W, int FM>
-__device__ __forceinline__ uint64_t warp_entry(const float *src, bool chan, const DecParams &p,
-                                               const FrameCtx &fc, int lh, const WarpCtx &wc, int d,
-                                               uint32_t j)
+// warp 0 decodes the node (d, j) of width W <= 256 whose values are at src
+// (or the channel when d == 0) and leaves its W partial-sum bits in sm.xs
+template <int FM, int V>
+__device__ __forceinline__ void warp_node(const float *src, bool chan, const DecParams &p, const FrameCtx &fc,
+                                          uint32_t lh, const WarpCtx &wc, uint32_t *xs, uint32_t pos)
 {
     const int lane = threadIdx.x & 31;
-    float v0 = 0.0f, v1 = 0.0f;
-    if (chan) {
-        if (lane < W) v0 = chan_load(p, fc, lane);
-        if (W == 64) v1 = chan_load(p, fc, 32 + lane);
+    float v[V];
+#pragma unroll
+    for (int q = 0; q < V; q++) v[q] = chan ? chan_load(p, fc, 32 * q + lane) : src[32 * q + lane];
+    uint32_t out[V];
+    if constexpr (V == 1) {
+        out[0] = engine32<FM>(v[0], lh, 32, wc);
     } else {
-        if (lane < W) v0 = src[lane];
-        if (W == 64) v1 = src[32 + lane];
+        wlevel<FM, V>(v, lh, wc, out);
     }
-    return wdec<W, FM>(v0, v1, lh, wc, d, j);
+    if (lane < V) {
+        uint32_t o = out[0];
+#pragma unroll
+        for (int q = 1; q < V; q++) o = lane == q ? out[q] : o;
+        xs[(pos >> 5) + lane] = o;
+    }
 }
 
 template <int FM>
-__global__ void __launch_bounds__(256) sc_decode_kernel(DecParams p)
+__device__ __forceinline__ void warp_small(const float *src, bool chan, const DecParams &p, const FrameCtx &fc,
+                                           uint32_t lh, const WarpCtx &wc, uint32_t *xs, uint32_t pos, int W)
+{
+    // W < 32 only happens for blocks shorter than 32 (the root itself)
+    const int lane = threadIdx.x & 31;
+    float v = 0.0f;
+    if (lane < W) v = chan ? chan_load(p, fc, lane) : src[lane];
+    const uint32_t bits = engine32<FM>(v, lh, W, wc);
+    if (lane == 0) put_bits(xs, pos, W, bits);
+}
+
+template <int FM>
+__global__ void __launch_bounds__(256, 1) sc_decode_kernel(DecParams p)
 {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     __shared__ float red[32];
@@ -429,14 +613,17 @@ __global__ void __launch_bounds__(256) sc_decode_kernel(DecParams p)
     fc.X = p.X + (size_t)frame * p.wpf;
     fc.dump = p.dump ? p.dump + (size_t)frame * (p.n + 1) * N : nullptr;
 
+    const int tid = threadIdx.x, nthr = blockDim.x;
+    const int dS = p.n - p.log2S;  // depth of the shared-memory sub-tree roots
+    const uint32_t WMAX = S < 256 ? S : 256;  // nodes this wide or narrower: one warp, registers
+
     WarpCtx wc;
     wc.ty = sm.ty;
     wc.dump = fc.dump;
     wc.N = N;
     wc.plain = p.plain;
-
-    const int tid = threadIdx.x, nthr = blockDim.x;
-    const int dS = p.n - p.log2S;  // depth of the shared-memory sub-tree roots
+    wc.dS = dS;
+    wc.jS = 0;
 
     if (fc.dump)
         for (uint32_t i = tid; i < N; i += nthr) fc.dump[i] = chan_load(p, fc, i);
@@ -492,6 +679,7 @@ __global__ void __launch_bounds__(256) sc_decode_kernel(DecParams p)
                 continue;
             }
             if (W == S) {
+                wc.jS = j;
                 PROF_MARK(PR_TYPES);
                 // entering a shared-memory sub-tree: stage its node types
                 __syncthreads();
@@ -500,7 +688,7 @@ __global__ void __launch_bounds__(256) sc_decode_kernel(DecParams p)
                     sm.ty[q] = __ldg(p.types + ((size_t)1 << (dS + e)) + ((size_t)j << e) + (q - (1u << e)));
                 }
             }
-            if (W <= 64) {
+            if (W <= WMAX) {
                 PROF_MARK(PR_WARP);
                 if (prof) pr_acc[PR_NODES_WARP]++;
                 __syncthreads();
@@ -508,18 +696,15 @@ __global__ void __launch_bounds__(256) sc_decode_kernel(DecParams p)
                     const bool chan = d == 0;
                     const float *src = chan ? nullptr : stage_ptr(p, fc, sm, W);
                     const int e = d - dS;
-                    const int lh = (1 << e) + (int)(j & ((1u << e) - 1u));
-                    uint64_t bits;
+                    const uint32_t lh = (1u << e) + (j & ((1u << e) - 1u));
+                    const uint32_t pos = (j * W) & (S - 1);
                     switch (W) {
-                    case 64: bits = warp_entry<64, FM>(src, chan, p, fc, lh, wc, d, j); break;
-                    case 32: bits = warp_entry<32, FM>(src, chan, p, fc, lh, wc, d, j); break;
-                    case 16: bits = warp_entry<16, FM>(src, chan, p, fc, lh, wc, d, j); break;
-                    case 8: bits = warp_entry<8, FM>(src, chan, p, fc, lh, wc, d, j); break;
-                    case 4: bits = warp_entry<4, FM>(src, chan, p, fc, lh, wc, d, j); break;
-                    case 2: bits = warp_entry<2, FM>(src, chan, p, fc, lh, wc, d, j); break;
-                    default: bits = warp_entry<1, FM>(src, chan, p, fc, lh, wc, d, j); break;
+                    case 256: warp_node<FM, 8>(src, chan, p, fc, lh, wc, sm.xs, pos); break;
+                    case 128: warp_node<FM, 4>(src, chan, p, fc, lh, wc, sm.xs, pos); break;
+                    case 64: warp_node<FM, 2>(src, chan, p, fc, lh, wc, sm.xs, pos); break;
+                    case 32: warp_node<FM, 1>(src, chan, p, fc, lh, wc, sm.xs, pos); break;
+                    default: warp_small<FM>(src, chan, p, fc, lh, wc, sm.xs, pos, (int)W); break;
                     }
-                    if (tid == 0) put_bits(sm.xs, (j * W) & (S - 1), W, bits);
                 }
                 entering = false;
                 continue;
