@@ -288,7 +288,7 @@ struct WarpCtx {
 // Decode the node at S-local heap index `root` (width W0 <= 32, A holds its
 // values: lane l = element l for l < W0).  Returns its W0 partial-sum bits.
 template <int FM>
-__device__ __forceinline__ uint32_t engine32(float A, uint32_t root, int W0, const WarpCtx &c)
+__device__ __noinline__ uint32_t engine32(float A, uint32_t root, int W0, const WarpCtx c)
 {
     const unsigned FULL = 0xffffffffu;
     const int lane = threadIdx.x & 31;
@@ -412,9 +412,15 @@ __device__ __forceinline__ uint32_t engine32(float A, uint32_t root, int W0, con
 
 // W = 32V node at S-local heap index lh; v[t] = element lane + 32t.
 // out[t] = partial-sum word t (bits of elements 32t .. 32t+31).
+template <int V> struct VecF { float x[V]; };
+template <int V> struct VecU { uint32_t x[V]; };
+
 template <int FM, int V>
-__device__ __forceinline__ void wlevel(const float (&v)[V], uint32_t lh, const WarpCtx &c, uint32_t (&out)[V])
+__device__ __noinline__ VecU<V> wlevel(const VecF<V> vin, uint32_t lh, const WarpCtx c)
 {
+    VecU<V> res;
+    uint32_t (&out)[V] = res.x;
+    const float (&v)[V] = vin.x;
     const unsigned FULL = 0xffffffffu;
     const int lane = threadIdx.x & 31;
     uint8_t t = c.ty[lh];
@@ -422,7 +428,7 @@ __device__ __forceinline__ void wlevel(const float (&v)[V], uint32_t lh, const W
     if (t == NT_RATE0) {
 #pragma unroll
         for (int q = 0; q < V; q++) out[q] = 0;
-        return;
+        return res;
     }
     if (t == NT_RATE1) {
         uint32_t m = 0x7f800000u;
@@ -432,7 +438,7 @@ __device__ __forceinline__ void wlevel(const float (&v)[V], uint32_t lh, const W
         if (rate1_guard(__uint_as_float(m), 5 + ilog2((uint32_t)V))) {
 #pragma unroll
             for (int q = 0; q < V; q++) out[q] = __ballot_sync(FULL, v[q] < 0.0f);
-            return;
+            return res;
         }
     }
     if (t == NT_REP) {
@@ -451,14 +457,15 @@ __device__ __forceinline__ void wlevel(const float (&v)[V], uint32_t lh, const W
         const float L = __shfl_sync(FULL, s0, 0);
 #pragma unroll
         for (int q = 0; q < V; q++) out[q] = L < 0.0f ? FULL : 0u;
-        return;
+        return res;
     }
     constexpr int H = V / 2;
     const int el = ilog2(lh);
     const int d = c.dS + el;
     const uint32_t j = (c.jS << el) + (lh - (1u << el));
     const uint32_t Wc = 32u * H;  // child width
-    float ch[H];
+    VecF<H> chv;
+    float (&ch)[H] = chv.x;
     uint32_t xl[H], xr[H];
     const bool skipl = !c.plain && c.ty[2 * lh] == NT_RATE0;
     if (skipl) {
@@ -470,8 +477,13 @@ __device__ __forceinline__ void wlevel(const float (&v)[V], uint32_t lh, const W
         if (c.dump)
 #pragma unroll
             for (int q = 0; q < H; q++) c.dump[(size_t)(d + 1) * c.N + (size_t)(2 * j) * Wc + 32 * q + lane] = ch[q];
-        if constexpr (H == 1) xl[0] = engine32<FM>(ch[0], 2 * lh, 32, c);
-        else wlevel<FM, H>(ch, 2 * lh, c, xl);
+        if constexpr (H == 1) {
+            xl[0] = engine32<FM>(ch[0], 2 * lh, 32, c);
+        } else {
+            const VecU<H> r = wlevel<FM, H>(chv, 2 * lh, c);
+#pragma unroll
+            for (int q = 0; q < H; q++) xl[q] = r.x[q];
+        }
     }
     const bool skipr = !c.plain && c.ty[2 * lh + 1] == NT_RATE0;
     if (skipr) {
@@ -484,14 +496,20 @@ __device__ __forceinline__ void wlevel(const float (&v)[V], uint32_t lh, const W
 #pragma unroll
             for (int q = 0; q < H; q++)
                 c.dump[(size_t)(d + 1) * c.N + (size_t)(2 * j + 1) * Wc + 32 * q + lane] = ch[q];
-        if constexpr (H == 1) xr[0] = engine32<FM>(ch[0], 2 * lh + 1, 32, c);
-        else wlevel<FM, H>(ch, 2 * lh + 1, c, xr);
+        if constexpr (H == 1) {
+            xr[0] = engine32<FM>(ch[0], 2 * lh + 1, 32, c);
+        } else {
+            const VecU<H> r = wlevel<FM, H>(chv, 2 * lh + 1, c);
+#pragma unroll
+            for (int q = 0; q < H; q++) xr[q] = r.x[q];
+        }
     }
 #pragma unroll
     for (int q = 0; q < H; q++) {
         out[q] = xl[q] ^ xr[q];
         out[H + q] = xr[q];
     }
+    return res;
 }
 
 // ---------------------------------------------------------------------------
@@ -561,14 +579,16 @@ __device__ __forceinline__ void warp_node(const float *src, bool chan, const Dec
                                           uint32_t lh, const WarpCtx &wc, uint32_t *xs, uint32_t pos)
 {
     const int lane = threadIdx.x & 31;
-    float v[V];
+    VecF<V> v;
 #pragma unroll
-    for (int q = 0; q < V; q++) v[q] = chan ? chan_load(p, fc, 32 * q + lane) : src[32 * q + lane];
+    for (int q = 0; q < V; q++) v.x[q] = chan ? chan_load(p, fc, 32 * q + lane) : src[32 * q + lane];
     uint32_t out[V];
     if constexpr (V == 1) {
-        out[0] = engine32<FM>(v[0], lh, 32, wc);
+        out[0] = engine32<FM>(v.x[0], lh, 32, wc);
     } else {
-        wlevel<FM, V>(v, lh, wc, out);
+        const VecU<V> r = wlevel<FM, V>(v, lh, wc);
+#pragma unroll
+        for (int q = 0; q < V; q++) out[q] = r.x[q];
     }
     if (lane < V) {
         uint32_t o = out[0];
@@ -749,6 +769,7 @@ __global__ void __launch_bounds__(256, 1) sc_decode_kernel(DecParams p)
             }
             float *dst = stage_ptr(p, fc, sm, H);
             float *dmp = fc.dump ? fc.dump + (size_t)(d + 1) * N + (size_t)(2 * j) * H : nullptr;
+#pragma unroll 1
             for (uint32_t i = tid; i < H; i += nthr) {
                 const float a = d == 0 ? chan_load(p, fc, i) : src[i];
                 const float b = d == 0 ? chan_load(p, fc, i + H) : src[i + H];
@@ -799,6 +820,7 @@ __global__ void __launch_bounds__(256, 1) sc_decode_kernel(DecParams p)
             const uint32_t lpos = xpos(W, j * W);
             float *dst = stage_ptr(p, fc, sm, W);
             float *dmp = fc.dump ? fc.dump + (size_t)d * N + (size_t)jr * W : nullptr;
+#pragma unroll 1
             for (uint32_t i = tid; i < W; i += nthr) {
                 const float a = d - 1 == 0 ? chan_load(p, fc, i) : src[i];
                 const float b = d - 1 == 0 ? chan_load(p, fc, i + W) : src[i + W];
