@@ -285,6 +285,65 @@ struct WarpCtx {
     uint32_t jS;         // its index
 };
 
+// Closed-form SC of a width-2 node with values (a, b) (uniform across the
+// warp): type t, leaf frozen flags fa, fb.  Returns its 2 partial-sum bits.
+template <int FM>
+__device__ __forceinline__ uint32_t sc_w2(float a, float b, uint32_t t, bool fa, bool fb, bool plain)
+{
+    if (!plain) {
+        if (t == NT_RATE0) return 0u;
+        if (t == NT_REP) return (b + a) < 0.0f ? 3u : 0u;
+        if (t == NT_RATE1 && rate1_guard(fminf(fabsf(a), fabsf(b)), 1))
+            return (a < 0.0f ? 1u : 0u) | (b < 0.0f ? 2u : 0u);
+    }
+    const uint32_t u0 = fa ? 0u : (pq_f<FM>(a, b) < 0.0f ? 1u : 0u);
+    const uint32_t u1 = fb ? 0u : (pq_g(a, b, u0) < 0.0f ? 1u : 0u);
+    return (u0 ^ u1) | (u1 << 1);
+}
+
+// Closed-form SC of a width-4 node whose values every lane holds (L0..L3):
+// no shuffles, no loop -- the four leaves of the node are decided in
+// registers.  t4: node type; tl/tr: types of its width-2 children; fz: leaf
+// frozen bits (bit i = leaf i).  In plain mode every stage LLR is dumped.
+template <int FM>
+__device__ __forceinline__ uint32_t sc_w4(float L0, float L1, float L2, float L3, uint32_t t4, uint32_t tl,
+                                          uint32_t tr, uint32_t fz, bool plain, float *dump, uint32_t N, int d,
+                                          uint32_t j)
+{
+    if (!plain) {
+        if (t4 == NT_RATE0) return 0u;
+        if (t4 == NT_RATE1 &&
+            rate1_guard(fminf(fminf(fabsf(L0), fabsf(L1)), fminf(fabsf(L2), fabsf(L3))), 2))
+            return (L0 < 0.0f ? 1u : 0u) | (L1 < 0.0f ? 2u : 0u) | (L2 < 0.0f ? 4u : 0u) | (L3 < 0.0f ? 8u : 0u);
+        if (t4 == NT_REP) return ((L3 + L1) + (L2 + L0)) < 0.0f ? 15u : 0u;
+    }
+    const bool lane0 = (threadIdx.x & 31) == 0;
+    uint32_t xl = 0, xr = 0;
+    if (plain || tl != NT_RATE0) {
+        const float l0 = pq_f<FM>(L0, L2), l1 = pq_f<FM>(L1, L3);
+        xl = sc_w2<FM>(l0, l1, tl, fz & 1u, fz & 2u, plain);
+        if (dump && lane0) {
+            const uint32_t u0 = ((fz & 1u) || pq_f<FM>(l0, l1) >= 0.0f) ? 0u : 1u;
+            dump[(size_t)(d + 1) * N + 4 * j + 0] = l0;
+            dump[(size_t)(d + 1) * N + 4 * j + 1] = l1;
+            dump[(size_t)(d + 2) * N + 4 * j + 0] = pq_f<FM>(l0, l1);
+            dump[(size_t)(d + 2) * N + 4 * j + 1] = pq_g(l0, l1, u0);
+        }
+    }
+    if (plain || tr != NT_RATE0) {
+        const float r0 = pq_g(L0, L2, xl & 1u), r1 = pq_g(L1, L3, (xl >> 1) & 1u);
+        xr = sc_w2<FM>(r0, r1, tr, fz & 4u, fz & 8u, plain);
+        if (dump && lane0) {
+            const uint32_t u2 = ((fz & 4u) || pq_f<FM>(r0, r1) >= 0.0f) ? 0u : 1u;
+            dump[(size_t)(d + 1) * N + 4 * j + 2] = r0;
+            dump[(size_t)(d + 1) * N + 4 * j + 3] = r1;
+            dump[(size_t)(d + 2) * N + 4 * j + 2] = pq_f<FM>(r0, r1);
+            dump[(size_t)(d + 2) * N + 4 * j + 3] = pq_g(r0, r1, u2);
+        }
+    }
+    return ((xl ^ xr) & 3u) | (xr << 2);
+}
+
 // Decode the node at S-local heap index `root` (width W0 <= 32, A holds its
 // values: lane l = element l for l < W0).  Returns its W0 partial-sum bits.
 template <int FM>
@@ -322,6 +381,18 @@ __device__ __noinline__ uint32_t engine32(float A, uint32_t root, int W0, const 
         const float P = e == 0 ? A : B;
         const int h = (1 << (e - e0)) + (int)j;  // engine-local heap index
         if (entering) {
+            if (w == 4) {
+                // the whole width-4 node in registers of every lane
+                const float L0 = __shfl_sync(FULL, P, o), L1 = __shfl_sync(FULL, P, o + 1);
+                const float L2 = __shfl_sync(FULL, P, o + 2), L3 = __shfl_sync(FULL, P, o + 3);
+                const uint32_t t4 = c.plain ? NT_MIXED : ntype(h);
+                const uint32_t tl = ntype(2 * h), tr = ntype(2 * h + 1);
+                const uint32_t fz = (leaf0 >> (4 * j)) & 15u;
+                xnode = sc_w4<FM>(L0, L1, L2, L3, t4, tl, tr, fz, c.plain != 0, c.dump, c.N,
+                                  d_root + e - e0, (j_root << (e - e0)) + j);
+                entering = false;
+                continue;
+            }
             if (w == 1) {
                 const float L = __shfl_sync(FULL, P, o);
                 xnode = ((leaf0 >> j) & 1u) ? 0u : (L < 0.0f ? 1u : 0u);
