@@ -283,202 +283,267 @@ struct WarpCtx {
     int plain;
     int dS;              // absolute depth of the S-sub-tree root
     uint32_t jS;         // its index
+    unsigned long long *prof;  // unused (kept for the profile layout)
 };
 
-// Closed-form SC of a width-2 node with values (a, b) (uniform across the
-// warp): type t, leaf frozen flags fa, fb.  Returns its 2 partial-sum bits.
-template <int FM>
-__device__ __forceinline__ uint32_t sc_w2(float a, float b, uint32_t t, bool fa, bool fb, bool plain)
+// Node types of one width-32 sub-tree as uniform bit masks, indexed by the
+// sub-tree-local heap index h (root h = 1, children 2h, 2h+1): internal
+// nodes h < 32 carry 2 type bits (tb0, tb1); leaves h = 32..63 carry the
+// frozen flag in `leaf` (bit h - 32).  Sub-trees narrower than 32 (blocks
+// shorter than 32 only) sit at the leftmost node of that width.
+struct TypeBits {
+    uint32_t tb0, tb1, leaf;
+};
+__device__ __forceinline__ uint32_t tget(const TypeBits &T, int h)
 {
-    if (!plain) {
-        if (t == NT_RATE0) return 0u;
-        if (t == NT_REP) return (b + a) < 0.0f ? 3u : 0u;
-        if (t == NT_RATE1 && rate1_guard(fminf(fabsf(a), fabsf(b)), 1))
-            return (a < 0.0f ? 1u : 0u) | (b < 0.0f ? 2u : 0u);
+    return ((T.tb0 >> h) & 1u) | (((T.tb1 >> h) & 1u) << 1);
+}
+
+// absolute position of a node, for the plain-mode stage dump
+struct NodePos {
+    float *dump;
+    uint32_t N;
+    int d;
+    uint32_t j;
+};
+__device__ __forceinline__ NodePos child_pos(const NodePos &p, int side)
+{
+    NodePos c = p;
+    c.d = p.d + 1;
+    c.j = 2 * p.j + side;
+    return c;
+}
+// write node values held in registers (lane 0 writes; every lane holds them)
+template <int W>
+__device__ __forceinline__ void dump_regs(const NodePos &p, const float (&x)[W])
+{
+    if (p.dump && (threadIdx.x & 31) == 0) {
+        float *o = p.dump + (size_t)p.d * p.N + (size_t)p.j * W;
+#pragma unroll
+        for (int i = 0; i < W; i++) o[i] = x[i];
     }
-    const uint32_t u0 = fa ? 0u : (pq_f<FM>(a, b) < 0.0f ? 1u : 0u);
-    const uint32_t u1 = fb ? 0u : (pq_g(a, b, u0) < 0.0f ? 1u : 0u);
+}
+// write node values held one per lane (lanes 0..W-1)
+__device__ __forceinline__ void dump_lanes(const NodePos &p, float v, int W)
+{
+    const int lane = threadIdx.x & 31;
+    if (p.dump && lane < W) p.dump[(size_t)p.d * p.N + (size_t)p.j * W + lane] = v;
+}
+
+// ---- closed forms: the node's values are in registers of every lane; the
+// whole sub-tree is decided without shuffles or loops (uniform branches only)
+
+template <int FM>
+__device__ __forceinline__ uint32_t dec2(float a, float b, const TypeBits &T, int h, bool plain, const NodePos &np)
+{
+    const uint32_t t = plain ? NT_MIXED : tget(T, h);
+    if (t == NT_RATE0) return 0u;
+    if (t == NT_REP) return (b + a) < 0.0f ? 3u : 0u;
+    if (t == NT_RATE1 && rate1_guard(fminf(fabsf(a), fabsf(b)), 1))
+        return (a < 0.0f ? 1u : 0u) | (b < 0.0f ? 2u : 0u);
+    const bool fa = (T.leaf >> (2 * h - 32)) & 1u, fb = (T.leaf >> (2 * h - 31)) & 1u;
+    const float l = pq_f<FM>(a, b);
+    const uint32_t u0 = fa ? 0u : (l < 0.0f ? 1u : 0u);
+    const float r = pq_g(a, b, u0);
+    const uint32_t u1 = fb ? 0u : (r < 0.0f ? 1u : 0u);
+    if (np.dump && (threadIdx.x & 31) == 0) {
+        np.dump[(size_t)(np.d + 1) * np.N + 2 * np.j] = l;
+        np.dump[(size_t)(np.d + 1) * np.N + 2 * np.j + 1] = r;
+    }
     return (u0 ^ u1) | (u1 << 1);
 }
 
-// Closed-form SC of a width-4 node whose values every lane holds (L0..L3):
-// no shuffles, no loop -- the four leaves of the node are decided in
-// registers.  t4: node type; tl/tr: types of its width-2 children; fz: leaf
-// frozen bits (bit i = leaf i).  In plain mode every stage LLR is dumped.
 template <int FM>
-__device__ __forceinline__ uint32_t sc_w4(float L0, float L1, float L2, float L3, uint32_t t4, uint32_t tl,
-                                          uint32_t tr, uint32_t fz, bool plain, float *dump, uint32_t N, int d,
-                                          uint32_t j)
+__device__ __forceinline__ uint32_t dec4(const float (&x)[4], const TypeBits &T, int h, bool plain,
+                                         const NodePos &np)
 {
-    if (!plain) {
-        if (t4 == NT_RATE0) return 0u;
-        if (t4 == NT_RATE1 &&
-            rate1_guard(fminf(fminf(fabsf(L0), fabsf(L1)), fminf(fabsf(L2), fabsf(L3))), 2))
-            return (L0 < 0.0f ? 1u : 0u) | (L1 < 0.0f ? 2u : 0u) | (L2 < 0.0f ? 4u : 0u) | (L3 < 0.0f ? 8u : 0u);
-        if (t4 == NT_REP) return ((L3 + L1) + (L2 + L0)) < 0.0f ? 15u : 0u;
-    }
-    const bool lane0 = (threadIdx.x & 31) == 0;
+    const uint32_t t = plain ? NT_MIXED : tget(T, h);
+    if (t == NT_RATE0) return 0u;
+    if (t == NT_RATE1 &&
+        rate1_guard(fminf(fminf(fabsf(x[0]), fabsf(x[1])), fminf(fabsf(x[2]), fabsf(x[3]))), 2))
+        return (x[0] < 0.0f ? 1u : 0u) | (x[1] < 0.0f ? 2u : 0u) | (x[2] < 0.0f ? 4u : 0u) |
+               (x[3] < 0.0f ? 8u : 0u);
+    if (t == NT_REP) return ((x[3] + x[1]) + (x[2] + x[0])) < 0.0f ? 15u : 0u;
     uint32_t xl = 0, xr = 0;
-    if (plain || tl != NT_RATE0) {
-        const float l0 = pq_f<FM>(L0, L2), l1 = pq_f<FM>(L1, L3);
-        xl = sc_w2<FM>(l0, l1, tl, fz & 1u, fz & 2u, plain);
-        if (dump && lane0) {
-            const uint32_t u0 = ((fz & 1u) || pq_f<FM>(l0, l1) >= 0.0f) ? 0u : 1u;
-            dump[(size_t)(d + 1) * N + 4 * j + 0] = l0;
-            dump[(size_t)(d + 1) * N + 4 * j + 1] = l1;
-            dump[(size_t)(d + 2) * N + 4 * j + 0] = pq_f<FM>(l0, l1);
-            dump[(size_t)(d + 2) * N + 4 * j + 1] = pq_g(l0, l1, u0);
-        }
+    float c[2];
+    if (plain || tget(T, 2 * h) != NT_RATE0) {
+        c[0] = pq_f<FM>(x[0], x[2]);
+        c[1] = pq_f<FM>(x[1], x[3]);
+        dump_regs<2>(child_pos(np, 0), c);
+        xl = dec2<FM>(c[0], c[1], T, 2 * h, plain, child_pos(np, 0));
     }
-    if (plain || tr != NT_RATE0) {
-        const float r0 = pq_g(L0, L2, xl & 1u), r1 = pq_g(L1, L3, (xl >> 1) & 1u);
-        xr = sc_w2<FM>(r0, r1, tr, fz & 4u, fz & 8u, plain);
-        if (dump && lane0) {
-            const uint32_t u2 = ((fz & 4u) || pq_f<FM>(r0, r1) >= 0.0f) ? 0u : 1u;
-            dump[(size_t)(d + 1) * N + 4 * j + 2] = r0;
-            dump[(size_t)(d + 1) * N + 4 * j + 3] = r1;
-            dump[(size_t)(d + 2) * N + 4 * j + 2] = pq_f<FM>(r0, r1);
-            dump[(size_t)(d + 2) * N + 4 * j + 3] = pq_g(r0, r1, u2);
-        }
+    if (plain || tget(T, 2 * h + 1) != NT_RATE0) {
+        c[0] = pq_g(x[0], x[2], xl & 1u);
+        c[1] = pq_g(x[1], x[3], (xl >> 1) & 1u);
+        dump_regs<2>(child_pos(np, 1), c);
+        xr = dec2<FM>(c[0], c[1], T, 2 * h + 1, plain, child_pos(np, 1));
     }
     return ((xl ^ xr) & 3u) | (xr << 2);
 }
 
-// Decode the node at S-local heap index `root` (width W0 <= 32, A holds its
-// values: lane l = element l for l < W0).  Returns its W0 partial-sum bits.
+template <int W> struct Regs { float x[W]; };
+
 template <int FM>
-__device__ __noinline__ uint32_t engine32(float A, uint32_t root, int W0, const WarpCtx c)
+__device__ __noinline__ uint32_t dec8(const Regs<8> xin, const TypeBits T, int h, bool plain, const NodePos np)
+{
+    const float (&x)[8] = xin.x;
+    const uint32_t t = plain ? NT_MIXED : tget(T, h);
+    if (t == NT_RATE0) return 0u;
+    if (t == NT_RATE1) {
+        float m = fabsf(x[0]);
+#pragma unroll
+        for (int i = 1; i < 8; i++) m = fminf(m, fabsf(x[i]));
+        if (rate1_guard(m, 3)) {
+            uint32_t bits = 0;
+#pragma unroll
+            for (int i = 0; i < 8; i++) bits |= (x[i] < 0.0f ? 1u : 0u) << i;
+            return bits;
+        }
+    }
+    if (t == NT_REP)
+        return (((x[7] + x[3]) + (x[5] + x[1])) + ((x[6] + x[2]) + (x[4] + x[0]))) < 0.0f ? 0xffu : 0u;
+    uint32_t xl = 0, xr = 0;
+    float c[4];
+    if (plain || tget(T, 2 * h) != NT_RATE0) {
+#pragma unroll
+        for (int i = 0; i < 4; i++) c[i] = pq_f<FM>(x[i], x[i + 4]);
+        dump_regs<4>(child_pos(np, 0), c);
+        xl = dec4<FM>(c, T, 2 * h, plain, child_pos(np, 0));
+    }
+    if (plain || tget(T, 2 * h + 1) != NT_RATE0) {
+#pragma unroll
+        for (int i = 0; i < 4; i++) c[i] = pq_g(x[i], x[i + 4], (xl >> i) & 1u);
+        dump_regs<4>(child_pos(np, 1), c);
+        xr = dec4<FM>(c, T, 2 * h + 1, plain, child_pos(np, 1));
+    }
+    return (xl ^ xr) | (xr << 4);
+}
+
+// ---- lane-parallel levels: lane i holds element i of a W = 16 / 32 node
+
+// rate-1 / repetition handling of a node held one element per lane (lanes < W)
+__device__ __forceinline__ bool lanes_special(float v, int W, uint32_t t, uint32_t &bits)
 {
     const unsigned FULL = 0xffffffffu;
     const int lane = threadIdx.x & 31;
-    const int e0 = 5 - ilog2((uint32_t)W0);
-    // fetch the sub-tree's node types: lane h (1 <= h < W0) internal node h,
-    // lane h (< W0) also the leaf W0 + h
-    uint32_t tint = NT_MIXED, tleaf = NT_RATE1;
-    {
-        const int eh = lane >= 1 ? ilog2((uint32_t)lane) : 0;
-        if (lane >= 1 && lane < W0) tint = c.ty[(root << eh) + (uint32_t)(lane - (1 << eh))];
-        const int el = ilog2((uint32_t)W0);
-        if (lane < W0) tleaf = c.ty[(root << el) + (uint32_t)lane];
+    if (t == NT_RATE0) {
+        bits = 0;
+        return true;
     }
-    if (c.plain) tint = NT_MIXED;
-    const uint32_t tb0 = __ballot_sync(FULL, tint & 1u), tb1 = __ballot_sync(FULL, tint & 2u);
-    const uint32_t leaf0 = __ballot_sync(FULL, tleaf == NT_RATE0);
-    auto ntype = [&](int h) -> uint32_t { return ((tb0 >> h) & 1u) | (((tb1 >> h) & 1u) << 1); };
-    // absolute node coordinates for the stage dump
-    const int el0 = ilog2(root);
-    const int d_root = c.dS + el0;
-    const uint32_t j_root = (c.jS << el0) + (root - (1u << el0));
+    if (t == NT_RATE1) {
+        uint32_t m = lane < W ? (__float_as_uint(v) & 0x7fffffffu) : 0x7f800000u;
+        m = __reduce_min_sync(FULL, m);
+        if (rate1_guard(__uint_as_float(m), ilog2((uint32_t)W))) {
+            bits = __ballot_sync(FULL, lane < W && v < 0.0f) & lowmask(W);
+            return true;
+        }
+    }
+    if (t == NT_REP) {
+        float sum = v;
+        for (int hh = W / 2; hh >= 1; hh >>= 1) {
+            const float other = __shfl_down_sync(FULL, sum, hh);
+            sum = other + sum;
+        }
+        bits = __shfl_sync(FULL, sum, 0) < 0.0f ? lowmask(W) : 0u;
+        return true;
+    }
+    return false;
+}
 
-    float B = A, Ca = 0.0f, Cb = 0.0f;
-    if (e0 > 0) B = __shfl_sync(FULL, A, (lane - eng_off(e0)) & 31);
-    int e = e0;
-    uint32_t j = 0, xnode = 0, XL = 0;
-    bool entering = true;
-    for (;;) {
-        const int w = 32 >> e;
-        const int o = eng_off(e);
-        const float P = e == 0 ? A : B;
-        const int h = (1 << (e - e0)) + (int)j;  // engine-local heap index
-        if (entering) {
-            if (w == 4) {
-                // the whole width-4 node in registers of every lane
-                const float L0 = __shfl_sync(FULL, P, o), L1 = __shfl_sync(FULL, P, o + 1);
-                const float L2 = __shfl_sync(FULL, P, o + 2), L3 = __shfl_sync(FULL, P, o + 3);
-                const uint32_t t4 = c.plain ? NT_MIXED : ntype(h);
-                const uint32_t tl = ntype(2 * h), tr = ntype(2 * h + 1);
-                const uint32_t fz = (leaf0 >> (4 * j)) & 15u;
-                xnode = sc_w4<FM>(L0, L1, L2, L3, t4, tl, tr, fz, c.plain != 0, c.dump, c.N,
-                                  d_root + e - e0, (j_root << (e - e0)) + j);
-                entering = false;
-                continue;
-            }
-            if (w == 1) {
-                const float L = __shfl_sync(FULL, P, o);
-                xnode = ((leaf0 >> j) & 1u) ? 0u : (L < 0.0f ? 1u : 0u);
-                entering = false;
-                continue;
-            }
-            const uint32_t t = ntype(h);
-            const bool in = lane >= o && lane < o + w;
-            if (t == NT_RATE0) {
-                xnode = 0;
-                entering = false;
-                continue;
-            }
-            if (t == NT_RATE1) {
-                uint32_t m = in ? (__float_as_uint(P) & 0x7fffffffu) : 0x7f800000u;
-                m = __reduce_min_sync(FULL, m);
-                if (rate1_guard(__uint_as_float(m), ilog2((uint32_t)w))) {
-                    xnode = (__ballot_sync(FULL, in && P < 0.0f) >> o) & lowmask(w);
-                    entering = false;
-                    continue;
-                }
-            }
-            if (t == NT_REP) {
-                // last-leaf LLR = SC's g-chain with zero partial sums, in SC's own
-                // pairing order: r_i = L[i + w/2] + L[i], halving down to one value
-                float sum = P;
-                for (int hh = w / 2; hh >= 1; hh >>= 1) {
-                    const float other = __shfl_down_sync(FULL, sum, hh);
-                    sum = other + sum;
-                }
-                const float L = __shfl_sync(FULL, sum, o);
-                xnode = L < 0.0f ? lowmask(w) : 0u;
-                entering = false;
-                continue;
-            }
-            // mixed: f-step into the left child (operands kept in Ca/Cb)
-            const int oc = eng_off(e + 1), hw = w / 2;
-            const int src = o + (lane - oc);
-            const float a = __shfl_sync(FULL, P, src & 31);
-            const float b = __shfl_sync(FULL, P, (src + hw) & 31);
-            const bool inc = lane >= oc && lane < oc + hw;
-            Ca = inc ? a : Ca;
-            Cb = inc ? b : Cb;
-            const bool lft0 = hw == 1 ? ((leaf0 >> (2 * j)) & 1u) != 0 : ntype(2 * h) == NT_RATE0;
-            if (lft0 && !c.plain) {
-                XL &= ~(lowmask(hw) << oc);  // left child decided: all zero
-                e++;
-                j = 2 * j;
-                xnode = 0;
-                entering = false;
-                continue;
-            }
-            const float fv = pq_f<FM>(a, b);
-            B = inc ? fv : B;
-            if (c.dump && inc)
-                c.dump[(size_t)(d_root + e - e0 + 1) * c.N + ((size_t)j_root << (e - e0 + 1)) * hw +
-                       (size_t)(2 * j) * hw + (lane - oc)] = fv;
-            e++;
-            j = 2 * j;
-            continue;
-        }
-        // node (e, j) is decided with partial sums xnode
-        if (e == e0) return xnode;
-        if ((j & 1u) == 0) {
-            XL = (XL & ~(lowmask(w) << o)) | (xnode << o);
-            const bool rgt0 = w == 1 ? ((leaf0 >> (j + 1)) & 1u) != 0 : ntype(h + 1) == NT_RATE0;
-            j++;
-            if (rgt0 && !c.plain) {
-                xnode = 0;
-                continue;  // right child decided too
-            }
-            const bool inc = lane >= o && lane < o + w;
-            const uint32_t sbit = (xnode >> ((lane - o) & 31)) & 1u;
-            const float gv = pq_g(Ca, Cb, sbit);
-            B = inc ? gv : B;
-            if (c.dump && inc)
-                c.dump[(size_t)(d_root + e - e0) * c.N + ((size_t)j_root << (e - e0)) * w + (size_t)j * w +
-                       (lane - o)] = gv;
-            entering = true;
-            continue;
-        }
-        const uint32_t xl = (XL >> o) & lowmask(w);
-        xnode = (xl ^ xnode) | (xnode << w);
-        e--;
-        j >>= 1;
+template <int FM>
+__device__ __forceinline__ Regs<8> gather8(float c)
+{
+    Regs<8> r;
+#pragma unroll
+    for (int i = 0; i < 8; i++) r.x[i] = __shfl_sync(0xffffffffu, c, i);
+    return r;
+}
+
+template <int FM>
+__device__ __forceinline__ uint32_t dec16(float v, const TypeBits &T, int h, bool plain, const NodePos &np)
+{
+    const int lane = threadIdx.x & 31;
+    uint32_t bits;
+    if (!plain && lanes_special(v, 16, tget(T, h), bits)) return bits;
+    const float b = __shfl_down_sync(0xffffffffu, v, 8);
+    uint32_t xl = 0, xr = 0;
+    if (plain || tget(T, 2 * h) != NT_RATE0) {
+        const float c = pq_f<FM>(v, b);
+        dump_lanes(child_pos(np, 0), c, 8);
+        xl = dec8<FM>(gather8<FM>(c), T, 2 * h, plain, child_pos(np, 0));
     }
+    if (plain || tget(T, 2 * h + 1) != NT_RATE0) {
+        const float c = pq_g(v, b, (xl >> (lane & 7)) & 1u);
+        dump_lanes(child_pos(np, 1), c, 8);
+        xr = dec8<FM>(gather8<FM>(c), T, 2 * h + 1, plain, child_pos(np, 1));
+    }
+    return (xl ^ xr) | (xr << 8);
+}
+
+template <int FM>
+__device__ __noinline__ uint32_t dec32(float v, const TypeBits T, bool plain, const NodePos np)
+{
+    const int lane = threadIdx.x & 31;
+    uint32_t bits;
+    if (!plain && lanes_special(v, 32, tget(T, 1), bits)) return bits;
+    const float b = __shfl_down_sync(0xffffffffu, v, 16);
+    uint32_t xl = 0, xr = 0;
+    if (plain || tget(T, 2) != NT_RATE0) {
+        const float c = pq_f<FM>(v, b);
+        dump_lanes(child_pos(np, 0), c, 16);
+        xl = dec16<FM>(c, T, 2, plain, child_pos(np, 0));
+    }
+    if (plain || tget(T, 3) != NT_RATE0) {
+        const float c = pq_g(v, b, (xl >> (lane & 15)) & 1u);
+        dump_lanes(child_pos(np, 1), c, 16);
+        xr = dec16<FM>(c, T, 3, plain, child_pos(np, 1));
+    }
+    return (xl ^ xr) | (xr << 16);
+}
+
+// Load the TypeBits of the node at S-local heap index `root`, width W0 <= 32.
+__device__ __forceinline__ TypeBits load_typebits(const uint8_t *ty, uint32_t root, int W0, bool plain)
+{
+    const unsigned FULL = 0xffffffffu;
+    const int lane = threadIdx.x & 31;
+    const int h0 = 32 / W0, k0 = ilog2((uint32_t)h0);
+    uint32_t tint = NT_MIXED;
+    if (lane >= h0) {
+        const int k = ilog2((uint32_t)lane) - k0;  // relative depth below the root
+        if (k >= 0 && (lane >> k) == h0) tint = ty[(root << k) + (uint32_t)(lane - (h0 << k))];
+    }
+    if (plain) tint = NT_MIXED;
+    const uint8_t tl = lane < W0 ? ty[(root << ilog2((uint32_t)W0)) + (uint32_t)lane] : NT_RATE1;
+    TypeBits T;
+    T.tb0 = __ballot_sync(FULL, tint & 1u);
+    T.tb1 = __ballot_sync(FULL, tint & 2u);
+    T.leaf = __ballot_sync(FULL, tl == NT_RATE0);
+    return T;
+}
+
+// Decode the node at S-local heap index `root` of width W0 <= 32 whose
+// values are held one per lane in A (lane l = element l).  Returns its bits.
+template <int FM>
+__device__ __forceinline__ uint32_t engine32(float A, uint32_t root, int W0, const WarpCtx c)
+{
+    const TypeBits T = load_typebits(c.ty, root, W0, c.plain != 0);
+    const int el = ilog2(root);
+    NodePos np;
+    np.dump = c.dump;
+    np.N = c.N;
+    np.d = c.dS + el;
+    np.j = (c.jS << el) + (root - (1u << el));
+    const bool plain = c.plain != 0;
+    if (W0 == 32) return dec32<FM>(A, T, plain, np);
+    if (W0 == 16) return dec16<FM>(A, T, 2, plain, np);
+    if (W0 == 8) return dec8<FM>(gather8<FM>(A), T, 4, plain, np);
+    float x[4];
+#pragma unroll
+    for (int i = 0; i < 4; i++) x[i] = __shfl_sync(0xffffffffu, A, i);
+    if (W0 == 4) return dec4<FM>(x, T, 8, plain, np);
+    if (W0 == 2) return dec2<FM>(x[0], x[1], T, 16, plain, np);
+    // W0 == 1: a single leaf
+    return ((T.leaf & 1u) || !(x[0] < 0.0f)) ? 0u : 1u;
 }
 
 // W = 32V node at S-local heap index lh; v[t] = element lane + 32t.
@@ -708,7 +773,10 @@ __global__ void __launch_bounds__(256, 1) sc_decode_kernel(DecParams p)
     const int dS = p.n - p.log2S;  // depth of the shared-memory sub-tree roots
     const uint32_t WMAX = S < 256 ? S : 256;  // nodes this wide or narrower: one warp, registers
 
+    __shared__ unsigned long long eng_prof[4];
+    if (tid < 4) eng_prof[tid] = 0;
     WarpCtx wc;
+    wc.prof = p.prof ? eng_prof : nullptr;
     wc.ty = sm.ty;
     wc.dump = fc.dump;
     wc.N = N;
@@ -870,6 +938,9 @@ __global__ void __launch_bounds__(256, 1) sc_decode_kernel(DecParams p)
             PROF_MARK(PR_SM_OTHER);
             if (prof) {
                 pr_acc[PR_TOTAL] = clock64() - pr_start;
+                pr_acc[12] = eng_prof[0];
+                pr_acc[13] = eng_prof[1];
+                pr_acc[14] = eng_prof[2];
                 for (int q = 0; q < PQ_PROF_SLOTS; q++) p.prof[(size_t)frame * PQ_PROF_SLOTS + q] = pr_acc[q];
             }
             break;

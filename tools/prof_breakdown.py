@@ -43,7 +43,7 @@ for key in a.configs:
         if q in (9,):
             continue
         v = pr[:, q].mean()
-        if q >= 10:
+        if q >= 10 and q != 12:
             print(f"   {name:16s} {v:12.0f}")
         else:
             print(f"   {name:16s} {v:12.0f} cycles  {100 * v / tot:5.1f}%")
