@@ -21,7 +21,7 @@ PQ_OPT_PROFILE = 4
 PQ_PROF_SLOTS = 16
 PROF_NAMES = ("upper_f", "upper_g", "upper_other", "smem_f", "smem_g", "smem_other", "warp_subtrees",
               "type_staging", "rate1_block", "total", "n_warp_subtrees", "n_block_nodes",
-              "engine_cycles", "engine_calls", "engine_iters")
+              "w32_cycles", "w32_calls", "unused")
 
 # every symbol include/polarsc.h declares (tests check the .so exports them)
 EXPORTS = (

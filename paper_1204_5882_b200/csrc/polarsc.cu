@@ -241,6 +241,27 @@ __device__ __forceinline__ float chan_load(const DecParams &p, const FrameCtx &f
     return c ? -v : v;
 }
 
+// four consecutive channel LLRs (i % 4 == 0), sign-flipped by the coset word
+__device__ __forceinline__ float4 chan_load4(const DecParams &p, const FrameCtx &fc, uint32_t i)
+{
+    const uint32_t c4 = fc.cw ? (__ldg(fc.cw + (i >> 5)) >> (i & 31)) & 15u : 0u;
+    float4 v;
+    if (fc.y) {
+        const uint32_t y4 = ((__ldg(fc.y + (i >> 5)) >> (i & 31)) & 15u) ^ c4;
+        v.x = (y4 & 1u) ? -p.mag : p.mag;
+        v.y = (y4 & 2u) ? -p.mag : p.mag;
+        v.z = (y4 & 4u) ? -p.mag : p.mag;
+        v.w = (y4 & 8u) ? -p.mag : p.mag;
+        return v;
+    }
+    v = __ldg(reinterpret_cast<const float4 *>(fc.llr + i));
+    v.x = __uint_as_float(__float_as_uint(v.x) ^ ((c4 & 1u) << 31));
+    v.y = __uint_as_float(__float_as_uint(v.y) ^ ((c4 & 2u) << 30));
+    v.z = __uint_as_float(__float_as_uint(v.z) ^ ((c4 & 4u) << 29));
+    v.w = __uint_as_float(__float_as_uint(v.w) ^ ((c4 & 8u) << 28));
+    return v;
+}
+
 // smem layout: [2S floats stage LLRs][SW words partial sums][2S bytes types]
 struct Smem {
     float *st;
@@ -283,8 +304,23 @@ struct WarpCtx {
     int plain;
     int dS;              // absolute depth of the S-sub-tree root
     uint32_t jS;         // its index
-    unsigned long long *prof;  // unused (kept for the profile layout)
+    unsigned long long *prof;  // shared {cycles in <=32-wide decoders, calls} or null
 };
+
+#ifdef PQ_UBENCH_TIMING
+__device__ unsigned long long g_ub_time[16], g_ub_count[16];
+#define UB_BEGIN() const long long ub_t0_ = clock64()
+#define UB_END(slot)                                                   \
+    do {                                                               \
+        if ((threadIdx.x & 31) == 0) {                                 \
+            g_ub_time[slot] += clock64() - ub_t0_;                     \
+            g_ub_count[slot] += 1;                                     \
+        }                                                              \
+    } while (0)
+#else
+#define UB_BEGIN()
+#define UB_END(slot)
+#endif
 
 // Node types of one width-32 sub-tree as uniform bit masks, indexed by the
 // sub-tree-local heap index h (root h = 1, children 2h, 2h+1): internal
@@ -384,7 +420,17 @@ __device__ __forceinline__ uint32_t dec4(const float (&x)[4], const TypeBits &T,
 template <int W> struct Regs { float x[W]; };
 
 template <int FM>
+__device__ __forceinline__ uint32_t dec8_body(const Regs<8> xin, const TypeBits T, int h, bool plain, const NodePos np);
+template <int FM>
 __device__ __noinline__ uint32_t dec8(const Regs<8> xin, const TypeBits T, int h, bool plain, const NodePos np)
+{
+    UB_BEGIN();
+    const uint32_t r = dec8_body<FM>(xin, T, h, plain, np);
+    UB_END(0);
+    return r;
+}
+template <int FM>
+__device__ __forceinline__ uint32_t dec8_body(const Regs<8> xin, const TypeBits T, int h, bool plain, const NodePos np)
 {
     const float (&x)[8] = xin.x;
     const uint32_t t = plain ? NT_MIXED : tget(T, h);
@@ -481,7 +527,17 @@ __device__ __forceinline__ uint32_t dec16(float v, const TypeBits &T, int h, boo
 }
 
 template <int FM>
+__device__ __forceinline__ uint32_t dec32_body(float v, const TypeBits T, bool plain, const NodePos np);
+template <int FM>
 __device__ __noinline__ uint32_t dec32(float v, const TypeBits T, bool plain, const NodePos np)
+{
+    UB_BEGIN();
+    const uint32_t r = dec32_body<FM>(v, T, plain, np);
+    UB_END(1);
+    return r;
+}
+template <int FM>
+__device__ __forceinline__ uint32_t dec32_body(float v, const TypeBits T, bool plain, const NodePos np)
 {
     const int lane = threadIdx.x & 31;
     uint32_t bits;
@@ -524,7 +580,7 @@ __device__ __forceinline__ TypeBits load_typebits(const uint8_t *ty, uint32_t ro
 // Decode the node at S-local heap index `root` of width W0 <= 32 whose
 // values are held one per lane in A (lane l = element l).  Returns its bits.
 template <int FM>
-__device__ __forceinline__ uint32_t engine32(float A, uint32_t root, int W0, const WarpCtx c)
+__device__ __forceinline__ uint32_t engine32_body(float A, uint32_t root, int W0, const WarpCtx c)
 {
     const TypeBits T = load_typebits(c.ty, root, W0, c.plain != 0);
     const int el = ilog2(root);
@@ -544,6 +600,18 @@ __device__ __forceinline__ uint32_t engine32(float A, uint32_t root, int W0, con
     if (W0 == 2) return dec2<FM>(x[0], x[1], T, 16, plain, np);
     // W0 == 1: a single leaf
     return ((T.leaf & 1u) || !(x[0] < 0.0f)) ? 0u : 1u;
+}
+
+template <int FM>
+__device__ __forceinline__ uint32_t engine32(float A, uint32_t root, int W0, const WarpCtx c)
+{
+    const long long pr_t0 = c.prof ? clock64() : 0;
+    const uint32_t r = engine32_body<FM>(A, root, W0, c);
+    if (c.prof && (threadIdx.x & 31) == 0) {
+        c.prof[0] += clock64() - pr_t0;
+        c.prof[1] += 1;
+    }
+    return r;
 }
 
 // W = 32V node at S-local heap index lh; v[t] = element lane + 32t.
@@ -747,7 +815,7 @@ __device__ __forceinline__ void warp_small(const float *src, bool chan, const De
 }
 
 template <int FM>
-__global__ void __launch_bounds__(256, 1) sc_decode_kernel(DecParams p)
+__global__ void __launch_bounds__(256, 2) sc_decode_kernel(DecParams p)
 {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     __shared__ float red[32];
@@ -908,13 +976,33 @@ __global__ void __launch_bounds__(256, 1) sc_decode_kernel(DecParams p)
             }
             float *dst = stage_ptr(p, fc, sm, H);
             float *dmp = fc.dump ? fc.dump + (size_t)(d + 1) * N + (size_t)(2 * j) * H : nullptr;
+            // f-step, 4 consecutive elements per thread and 2 float4 chunks in flight
+            // (H >= 256 here, so every chunk is a whole float4)
+            const bool ch0 = d == 0;
 #pragma unroll 1
-            for (uint32_t i = tid; i < H; i += nthr) {
-                const float a = d == 0 ? chan_load(p, fc, i) : src[i];
-                const float b = d == 0 ? chan_load(p, fc, i + H) : src[i + H];
-                const float v = pq_f<FM>(a, b);
-                dst[i] = v;
-                if (dmp) dmp[i] = v;
+            for (uint32_t base = 0; base < H; base += 8 * nthr) {
+                float4 a[2], b[2];
+#pragma unroll
+                for (int k = 0; k < 2; k++) {
+                    const uint32_t i = base + 4 * (tid + k * nthr);
+                    if (i < H) {
+                        a[k] = ch0 ? chan_load4(p, fc, i) : *reinterpret_cast<const float4 *>(src + i);
+                        b[k] = ch0 ? chan_load4(p, fc, i + H) : *reinterpret_cast<const float4 *>(src + i + H);
+                    }
+                }
+#pragma unroll
+                for (int k = 0; k < 2; k++) {
+                    const uint32_t i = base + 4 * (tid + k * nthr);
+                    if (i < H) {
+                        float4 v;
+                        v.x = pq_f<FM>(a[k].x, b[k].x);
+                        v.y = pq_f<FM>(a[k].y, b[k].y);
+                        v.z = pq_f<FM>(a[k].z, b[k].z);
+                        v.w = pq_f<FM>(a[k].w, b[k].w);
+                        *reinterpret_cast<float4 *>(dst + i) = v;
+                        if (dmp) *reinterpret_cast<float4 *>(dmp + i) = v;
+                    }
+                }
             }
             d++;
             j = 2 * j;
@@ -962,13 +1050,34 @@ __global__ void __launch_bounds__(256, 1) sc_decode_kernel(DecParams p)
             const uint32_t lpos = xpos(W, j * W);
             float *dst = stage_ptr(p, fc, sm, W);
             float *dmp = fc.dump ? fc.dump + (size_t)d * N + (size_t)jr * W : nullptr;
+            const bool ch0 = d - 1 == 0;
+            // g-step: W >= 256 here; 4 elements per thread, 4 chunks in flight
 #pragma unroll 1
-            for (uint32_t i = tid; i < W; i += nthr) {
-                const float a = d - 1 == 0 ? chan_load(p, fc, i) : src[i];
-                const float b = d - 1 == 0 ? chan_load(p, fc, i + W) : src[i + W];
-                const float v = pq_g(a, b, get_bit(xl, lpos + i));
-                dst[i] = v;
-                if (dmp) dmp[i] = v;
+            for (uint32_t base = 0; base < W; base += 16 * nthr) {
+                float4 a[4], b[4];
+                uint32_t sb[4];
+#pragma unroll
+                for (int k = 0; k < 4; k++) {
+                    const uint32_t i = base + 4 * (tid + k * nthr);
+                    if (i < W) {
+                        a[k] = ch0 ? chan_load4(p, fc, i) : *reinterpret_cast<const float4 *>(src + i);
+                        b[k] = ch0 ? chan_load4(p, fc, i + W) : *reinterpret_cast<const float4 *>(src + i + W);
+                        sb[k] = (xl[(lpos + i) >> 5] >> ((lpos + i) & 31)) & 15u;
+                    }
+                }
+#pragma unroll
+                for (int k = 0; k < 4; k++) {
+                    const uint32_t i = base + 4 * (tid + k * nthr);
+                    if (i < W) {
+                        float4 v;
+                        v.x = pq_g(a[k].x, b[k].x, sb[k] & 1u);
+                        v.y = pq_g(a[k].y, b[k].y, sb[k] & 2u);
+                        v.z = pq_g(a[k].z, b[k].z, sb[k] & 4u);
+                        v.w = pq_g(a[k].w, b[k].w, sb[k] & 8u);
+                        *reinterpret_cast<float4 *>(dst + i) = v;
+                        if (dmp) *reinterpret_cast<float4 *>(dmp + i) = v;
+                    }
+                }
             }
             j = jr;
             entering = true;

@@ -1,5 +1,6 @@
 // Microbenchmarks of the decoder's building blocks (includes the product source).
 // nvcc -gencode arch=compute_100a,code=sm_100a -O3 --fmad=false -std=c++17 -I../../include -o engine_bench engine_bench.cu
+#define PQ_UBENCH_TIMING 1
 #include "../../paper_1204_5882_b200/csrc/polarsc.cu"
 
 __global__ void k_f_latency(const float *in, float *out, int iters, long long *cyc)
@@ -41,6 +42,7 @@ __global__ void k_engine(const float *in, const uint8_t *ty_g, float *out, int i
     c.plain = plain;
     c.dS = 0;
     c.jS = 0;
+    c.prof = nullptr;
     float v = in[threadIdx.x];
     uint32_t acc = 0;
     long long t0 = clock64();
@@ -51,6 +53,36 @@ __global__ void k_engine(const float *in, const uint8_t *ty_g, float *out, int i
     long long t1 = clock64();
     out[threadIdx.x] = v + (float)acc;
     if (threadIdx.x == 0) cyc[0] = t1 - t0;
+}
+
+// one warp decodes the four W=256 sub-trees of the c1 code (S = N = 1024)
+__global__ void k_c1_warp(const uint8_t *types_g, const float *llr, long long *cyc, uint32_t *out)
+{
+    __shared__ uint8_t ty[2048];
+    load_log_table();
+    for (int i = threadIdx.x; i < 2048; i += 32) ty[i] = types_g[i];
+    __syncthreads();
+    WarpCtx c;
+    c.ty = ty;
+    c.dump = nullptr;
+    c.N = 1024;
+    c.plain = 0;
+    c.dS = 0;
+    c.jS = 0;
+    c.prof = nullptr;
+    const int lane = threadIdx.x & 31;
+    long long t0 = clock64();
+    uint32_t acc = 0;
+    for (int rep = 0; rep < 10; rep++)
+        for (int s = 0; s < 4; s++) {
+            VecF<8> v;
+            for (int q = 0; q < 8; q++) v.x[q] = llr[256 * s + 32 * q + lane] + 0.001f * (float)rep;
+            const VecU<8> r = wlevel<PQ_F_EXACT, 8>(v, 4 + s, c);
+            acc ^= r.x[0] ^ r.x[7];
+        }
+    long long t1 = clock64();
+    out[lane] = acc;
+    if (lane == 0) cyc[0] = (t1 - t0) / 10;
 }
 
 int main()
@@ -77,7 +109,42 @@ int main()
     for (int i = 0; i < 64; i++) t[i] = i < 32 ? NT_MIXED : ((i & 1) ? NT_RATE1 : NT_RATE0);
     cudaMemcpy(ty, t, 64, cudaMemcpyHostToDevice);
     for (int r = 0; r < 2; r++) k_engine<<<1, 32>>>(in, ty, out, 200, 1, cyc);
+    {
+        unsigned long long z[16] = {0};
+        cudaMemcpyToSymbol(g_ub_time, z, sizeof z);
+        cudaMemcpyToSymbol(g_ub_count, z, sizeof z);
+    }
     cudaMemcpy(&c, cyc, 8, cudaMemcpyDeviceToHost);
     printf("engine32 plain (31 mixed nodes): %.0f cycles/call = %.1f per node\n", (double)c / 200, (double)c / 200 / 31);
+    {
+        uint8_t *tyh = (uint8_t *)malloc(2048);
+        FILE *fp = fopen("tools/ubench/c1_types.bin", "rb");
+        if (fp) {
+            fread(tyh, 1, 2048, fp);
+            fclose(fp);
+            float *lh = (float *)malloc(4096);
+            uint32_t seed = 1;
+            for (int i = 0; i < 1024; i++) {
+                seed = seed * 1664525u + 1013904223u;
+                lh[i] = ((seed >> 8) & 1 ? 1.0f : -1.0f) * (0.5f + 3.0f * ((seed >> 9) & 1023) / 1023.0f);
+            }
+            float *dl;
+            uint8_t *dty;
+            uint32_t *dout;
+            cudaMalloc(&dl, 4096);
+            cudaMalloc(&dty, 2048);
+            cudaMalloc(&dout, 128);
+            cudaMemcpy(dl, lh, 4096, cudaMemcpyHostToDevice);
+            cudaMemcpy(dty, tyh, 2048, cudaMemcpyHostToDevice);
+            for (int r = 0; r < 2; r++) k_c1_warp<<<1, 32>>>(dty, dl, cyc, dout);
+            cudaMemcpy(&c, cyc, 8, cudaMemcpyDeviceToHost);
+            printf("c1 warp levels (4 x W256 sub-trees): %lld cycles\n", c);
+            unsigned long long tt[16], cc[16];
+            cudaMemcpyFromSymbol(tt, g_ub_time, sizeof tt);
+            cudaMemcpyFromSymbol(cc, g_ub_count, sizeof cc);
+            printf("dec8: %llu calls %.0f cycles/call; dec32: %llu calls %.0f cycles/call\n", cc[0],
+                   (double)tt[0] / (cc[0] ? cc[0] : 1), cc[1], (double)tt[1] / (cc[1] ? cc[1] : 1));
+        }
+    }
     printf("err=%s\n", cudaGetErrorString(cudaGetLastError()));
 }
