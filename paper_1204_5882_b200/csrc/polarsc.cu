@@ -389,82 +389,6 @@ __device__ __forceinline__ uint32_t dec2(float a, float b, const TypeBits &T, in
     return (u0 ^ u1) | (u1 << 1);
 }
 
-template <int FM>
-__device__ __forceinline__ uint32_t dec4(const float (&x)[4], const TypeBits &T, int h, bool plain,
-                                         const NodePos &np)
-{
-    const uint32_t t = plain ? NT_MIXED : tget(T, h);
-    if (t == NT_RATE0) return 0u;
-    if (t == NT_RATE1 &&
-        rate1_guard(fminf(fminf(fabsf(x[0]), fabsf(x[1])), fminf(fabsf(x[2]), fabsf(x[3]))), 2))
-        return (x[0] < 0.0f ? 1u : 0u) | (x[1] < 0.0f ? 2u : 0u) | (x[2] < 0.0f ? 4u : 0u) |
-               (x[3] < 0.0f ? 8u : 0u);
-    if (t == NT_REP) return ((x[3] + x[1]) + (x[2] + x[0])) < 0.0f ? 15u : 0u;
-    uint32_t xl = 0, xr = 0;
-    float c[2];
-    if (plain || tget(T, 2 * h) != NT_RATE0) {
-        c[0] = pq_f<FM>(x[0], x[2]);
-        c[1] = pq_f<FM>(x[1], x[3]);
-        dump_regs<2>(child_pos(np, 0), c);
-        xl = dec2<FM>(c[0], c[1], T, 2 * h, plain, child_pos(np, 0));
-    }
-    if (plain || tget(T, 2 * h + 1) != NT_RATE0) {
-        c[0] = pq_g(x[0], x[2], xl & 1u);
-        c[1] = pq_g(x[1], x[3], (xl >> 1) & 1u);
-        dump_regs<2>(child_pos(np, 1), c);
-        xr = dec2<FM>(c[0], c[1], T, 2 * h + 1, plain, child_pos(np, 1));
-    }
-    return ((xl ^ xr) & 3u) | (xr << 2);
-}
-
-template <int W> struct Regs { float x[W]; };
-
-template <int FM>
-__device__ __forceinline__ uint32_t dec8_body(const Regs<8> xin, const TypeBits T, int h, bool plain, const NodePos np);
-template <int FM>
-__device__ __noinline__ uint32_t dec8(const Regs<8> xin, const TypeBits T, int h, bool plain, const NodePos np)
-{
-    UB_BEGIN();
-    const uint32_t r = dec8_body<FM>(xin, T, h, plain, np);
-    UB_END(0);
-    return r;
-}
-template <int FM>
-__device__ __forceinline__ uint32_t dec8_body(const Regs<8> xin, const TypeBits T, int h, bool plain, const NodePos np)
-{
-    const float (&x)[8] = xin.x;
-    const uint32_t t = plain ? NT_MIXED : tget(T, h);
-    if (t == NT_RATE0) return 0u;
-    if (t == NT_RATE1) {
-        float m = fabsf(x[0]);
-#pragma unroll
-        for (int i = 1; i < 8; i++) m = fminf(m, fabsf(x[i]));
-        if (rate1_guard(m, 3)) {
-            uint32_t bits = 0;
-#pragma unroll
-            for (int i = 0; i < 8; i++) bits |= (x[i] < 0.0f ? 1u : 0u) << i;
-            return bits;
-        }
-    }
-    if (t == NT_REP)
-        return (((x[7] + x[3]) + (x[5] + x[1])) + ((x[6] + x[2]) + (x[4] + x[0]))) < 0.0f ? 0xffu : 0u;
-    uint32_t xl = 0, xr = 0;
-    float c[4];
-    if (plain || tget(T, 2 * h) != NT_RATE0) {
-#pragma unroll
-        for (int i = 0; i < 4; i++) c[i] = pq_f<FM>(x[i], x[i + 4]);
-        dump_regs<4>(child_pos(np, 0), c);
-        xl = dec4<FM>(c, T, 2 * h, plain, child_pos(np, 0));
-    }
-    if (plain || tget(T, 2 * h + 1) != NT_RATE0) {
-#pragma unroll
-        for (int i = 0; i < 4; i++) c[i] = pq_g(x[i], x[i + 4], (xl >> i) & 1u);
-        dump_regs<4>(child_pos(np, 1), c);
-        xr = dec4<FM>(c, T, 2 * h + 1, plain, child_pos(np, 1));
-    }
-    return (xl ^ xr) | (xr << 4);
-}
-
 // ---- lane-parallel levels: lane i holds element i of a W = 16 / 32 node
 
 // rate-1 / repetition handling of a node held one element per lane (lanes < W)
@@ -496,13 +420,58 @@ __device__ __forceinline__ bool lanes_special(float v, int W, uint32_t t, uint32
     return false;
 }
 
+
+// W = 4 node, lane i holds element i (lanes 0..3): lane-parallel f/g, the two
+// width-2 children decided in closed form in every lane's registers.
 template <int FM>
-__device__ __forceinline__ Regs<8> gather8(float c)
+__device__ __forceinline__ uint32_t dec4(float v, const TypeBits &T, int h, bool plain, const NodePos &np)
 {
-    Regs<8> r;
-#pragma unroll
-    for (int i = 0; i < 8; i++) r.x[i] = __shfl_sync(0xffffffffu, c, i);
-    return r;
+    const unsigned FULL = 0xffffffffu;
+    uint32_t bits;
+    if (!plain && lanes_special(v, 4, tget(T, h), bits)) return bits;
+    const float b = __shfl_down_sync(FULL, v, 2);
+    uint32_t xl = 0, xr = 0;
+    if (plain || tget(T, 2 * h) != NT_RATE0) {
+        const float c = pq_f<FM>(v, b);
+        const float c0 = __shfl_sync(FULL, c, 0), c1 = __shfl_sync(FULL, c, 1);
+        dump_lanes(child_pos(np, 0), c, 2);
+        xl = dec2<FM>(c0, c1, T, 2 * h, plain, child_pos(np, 0));
+    }
+    if (plain || tget(T, 2 * h + 1) != NT_RATE0) {
+        const float c = pq_g(v, b, (xl >> ((threadIdx.x & 31) & 1)) & 1u);
+        const float c0 = __shfl_sync(FULL, c, 0), c1 = __shfl_sync(FULL, c, 1);
+        dump_lanes(child_pos(np, 1), c, 2);
+        xr = dec2<FM>(c0, c1, T, 2 * h + 1, plain, child_pos(np, 1));
+    }
+    return ((xl ^ xr) & 3u) | (xr << 2);
+}
+
+// W = 8 node, lane i holds element i (lanes 0..7).  One copy (noinline).
+template <int FM>
+__device__ __noinline__ uint32_t dec8(float v, const TypeBits T, int h, bool plain, const NodePos np)
+{
+    UB_BEGIN();
+    const unsigned FULL = 0xffffffffu;
+    const int lane = threadIdx.x & 31;
+    uint32_t bits;
+    if (!plain && lanes_special(v, 8, tget(T, h), bits)) {
+        UB_END(0);
+        return bits;
+    }
+    const float b = __shfl_down_sync(FULL, v, 4);
+    uint32_t xl = 0, xr = 0;
+    if (plain || tget(T, 2 * h) != NT_RATE0) {
+        const float c = pq_f<FM>(v, b);
+        dump_lanes(child_pos(np, 0), c, 4);
+        xl = dec4<FM>(c, T, 2 * h, plain, child_pos(np, 0));
+    }
+    if (plain || tget(T, 2 * h + 1) != NT_RATE0) {
+        const float c = pq_g(v, b, (xl >> (lane & 3)) & 1u);
+        dump_lanes(child_pos(np, 1), c, 4);
+        xr = dec4<FM>(c, T, 2 * h + 1, plain, child_pos(np, 1));
+    }
+    UB_END(0);
+    return (xl ^ xr) | (xr << 4);
 }
 
 template <int FM>
@@ -516,12 +485,12 @@ __device__ __forceinline__ uint32_t dec16(float v, const TypeBits &T, int h, boo
     if (plain || tget(T, 2 * h) != NT_RATE0) {
         const float c = pq_f<FM>(v, b);
         dump_lanes(child_pos(np, 0), c, 8);
-        xl = dec8<FM>(gather8<FM>(c), T, 2 * h, plain, child_pos(np, 0));
+        xl = dec8<FM>(c, T, 2 * h, plain, child_pos(np, 0));
     }
     if (plain || tget(T, 2 * h + 1) != NT_RATE0) {
         const float c = pq_g(v, b, (xl >> (lane & 7)) & 1u);
         dump_lanes(child_pos(np, 1), c, 8);
-        xr = dec8<FM>(gather8<FM>(c), T, 2 * h + 1, plain, child_pos(np, 1));
+        xr = dec8<FM>(c, T, 2 * h + 1, plain, child_pos(np, 1));
     }
     return (xl ^ xr) | (xr << 8);
 }
@@ -592,11 +561,11 @@ __device__ __forceinline__ uint32_t engine32_body(float A, uint32_t root, int W0
     const bool plain = c.plain != 0;
     if (W0 == 32) return dec32<FM>(A, T, plain, np);
     if (W0 == 16) return dec16<FM>(A, T, 2, plain, np);
-    if (W0 == 8) return dec8<FM>(gather8<FM>(A), T, 4, plain, np);
+    if (W0 == 8) return dec8<FM>(A, T, 4, plain, np);
+    if (W0 == 4) return dec4<FM>(A, T, 8, plain, np);
     float x[4];
 #pragma unroll
-    for (int i = 0; i < 4; i++) x[i] = __shfl_sync(0xffffffffu, A, i);
-    if (W0 == 4) return dec4<FM>(x, T, 8, plain, np);
+    for (int i = 0; i < 2; i++) x[i] = __shfl_sync(0xffffffffu, A, i);
     if (W0 == 2) return dec2<FM>(x[0], x[1], T, 16, plain, np);
     // W0 == 1: a single leaf
     return ((T.leaf & 1u) || !(x[0] < 0.0f)) ? 0u : 1u;
@@ -612,108 +581,6 @@ __device__ __forceinline__ uint32_t engine32(float A, uint32_t root, int W0, con
         c.prof[1] += 1;
     }
     return r;
-}
-
-// W = 32V node at S-local heap index lh; v[t] = element lane + 32t.
-// out[t] = partial-sum word t (bits of elements 32t .. 32t+31).
-template <int V> struct VecF { float x[V]; };
-template <int V> struct VecU { uint32_t x[V]; };
-
-template <int FM, int V>
-__device__ __noinline__ VecU<V> wlevel(const VecF<V> vin, uint32_t lh, const WarpCtx c)
-{
-    VecU<V> res;
-    uint32_t (&out)[V] = res.x;
-    const float (&v)[V] = vin.x;
-    const unsigned FULL = 0xffffffffu;
-    const int lane = threadIdx.x & 31;
-    uint8_t t = c.ty[lh];
-    if (c.plain) t = NT_MIXED;
-    if (t == NT_RATE0) {
-#pragma unroll
-        for (int q = 0; q < V; q++) out[q] = 0;
-        return res;
-    }
-    if (t == NT_RATE1) {
-        uint32_t m = 0x7f800000u;
-#pragma unroll
-        for (int q = 0; q < V; q++) m = min(m, __float_as_uint(v[q]) & 0x7fffffffu);
-        m = __reduce_min_sync(FULL, m);
-        if (rate1_guard(__uint_as_float(m), 5 + ilog2((uint32_t)V))) {
-#pragma unroll
-            for (int q = 0; q < V; q++) out[q] = __ballot_sync(FULL, v[q] < 0.0f);
-            return res;
-        }
-    }
-    if (t == NT_REP) {
-        float sum[V];
-#pragma unroll
-        for (int q = 0; q < V; q++) sum[q] = v[q];
-#pragma unroll
-        for (int hv = V / 2; hv >= 1; hv >>= 1)
-#pragma unroll
-            for (int q = 0; q < hv; q++) sum[q] = sum[q + hv] + sum[q];
-        float s0 = sum[0];
-        for (int hh = 16; hh >= 1; hh >>= 1) {
-            const float other = __shfl_down_sync(FULL, s0, hh);
-            s0 = other + s0;
-        }
-        const float L = __shfl_sync(FULL, s0, 0);
-#pragma unroll
-        for (int q = 0; q < V; q++) out[q] = L < 0.0f ? FULL : 0u;
-        return res;
-    }
-    constexpr int H = V / 2;
-    const int el = ilog2(lh);
-    const int d = c.dS + el;
-    const uint32_t j = (c.jS << el) + (lh - (1u << el));
-    const uint32_t Wc = 32u * H;  // child width
-    VecF<H> chv;
-    float (&ch)[H] = chv.x;
-    uint32_t xl[H], xr[H];
-    const bool skipl = !c.plain && c.ty[2 * lh] == NT_RATE0;
-    if (skipl) {
-#pragma unroll
-        for (int q = 0; q < H; q++) xl[q] = 0;
-    } else {
-#pragma unroll
-        for (int q = 0; q < H; q++) ch[q] = pq_f<FM>(v[q], v[q + H]);
-        if (c.dump)
-#pragma unroll
-            for (int q = 0; q < H; q++) c.dump[(size_t)(d + 1) * c.N + (size_t)(2 * j) * Wc + 32 * q + lane] = ch[q];
-        if constexpr (H == 1) {
-            xl[0] = engine32<FM>(ch[0], 2 * lh, 32, c);
-        } else {
-            const VecU<H> r = wlevel<FM, H>(chv, 2 * lh, c);
-#pragma unroll
-            for (int q = 0; q < H; q++) xl[q] = r.x[q];
-        }
-    }
-    const bool skipr = !c.plain && c.ty[2 * lh + 1] == NT_RATE0;
-    if (skipr) {
-#pragma unroll
-        for (int q = 0; q < H; q++) xr[q] = 0;
-    } else {
-#pragma unroll
-        for (int q = 0; q < H; q++) ch[q] = pq_g(v[q], v[q + H], (xl[q] >> lane) & 1u);
-        if (c.dump)
-#pragma unroll
-            for (int q = 0; q < H; q++)
-                c.dump[(size_t)(d + 1) * c.N + (size_t)(2 * j + 1) * Wc + 32 * q + lane] = ch[q];
-        if constexpr (H == 1) {
-            xr[0] = engine32<FM>(ch[0], 2 * lh + 1, 32, c);
-        } else {
-            const VecU<H> r = wlevel<FM, H>(chv, 2 * lh + 1, c);
-#pragma unroll
-            for (int q = 0; q < H; q++) xr[q] = r.x[q];
-        }
-    }
-#pragma unroll
-    for (int q = 0; q < H; q++) {
-        out[q] = xl[q] ^ xr[q];
-        out[H + q] = xr[q];
-    }
-    return res;
 }
 
 // ---------------------------------------------------------------------------
@@ -776,29 +643,155 @@ __device__ __forceinline__ float block_min(float v, float *red)
 // ---------------------------------------------------------------------------
 // the per-frame tree walk
 
-// warp 0 decodes the node (d, j) of width W <= 256 whose values are at src
-// (or the channel when d == 0) and leaves its W partial-sum bits in sm.xs
-template <int FM, int V>
-__device__ __forceinline__ void warp_node(const float *src, bool chan, const DecParams &p, const FrameCtx &fc,
-                                          uint32_t lh, const WarpCtx &wc, uint32_t *xs, uint32_t pos)
+// One warp decodes the sub-tree rooted at (d0, j0), width 32 <= W0 <= 256,
+// inside the shared-memory sub-tree: node values in the shared stage buffers
+// (width W at st_end - 2W), partial sums in xs (bit position (jW) mod S).
+// Nodes of width 32 go to the register decoder dec32; wider ones take
+// warp-synchronous f/g steps (<= 4 elements per lane, independent f's in
+// flight).  Everything else (types, R0/R1/REP shortcuts, partial-sum XORs)
+// mirrors the block walk, with __syncwarp instead of __syncthreads.
+template <int FM>
+__device__ __noinline__ void warp_walk(float *st_end, uint32_t *xs, const uint8_t *ty, float *dump, uint32_t N,
+                                       uint32_t S, int dS, uint32_t jS, int plain_i, int d0, uint32_t j0)
 {
+    const unsigned FULL = 0xffffffffu;
     const int lane = threadIdx.x & 31;
-    VecF<V> v;
+    const bool plain = plain_i != 0;
+    int d = d0;
+    uint32_t j = j0;
+    bool entering = true;
+    for (;;) {
+        const uint32_t W = N >> d;
+        float *nd = st_end - 2 * W;
+        const int e = d - dS;
+        const uint32_t lh = (1u << e) + (j & ((1u << e) - 1u));
+        const uint32_t pos = (j * W) & (S - 1);
+        if (entering) {
+            const uint8_t t = plain ? NT_MIXED : ty[lh];
+            if (t == NT_RATE0) {
+                for (uint32_t w = lane; w < W / 32; w += 32) xs[(pos >> 5) + w] = 0;
+                __syncwarp();
+                entering = false;
+                continue;
+            }
+            if (W == 32) {
+                const float v = nd[lane];
+                const TypeBits T = load_typebits(ty, lh, 32, plain);
+                NodePos np;
+                np.dump = dump;
+                np.N = N;
+                np.d = d;
+                np.j = j;
+                const uint32_t bits = dec32<FM>(v, T, plain, np);
+                if (lane == 0) xs[pos >> 5] = bits;
+                __syncwarp();
+                entering = false;
+                continue;
+            }
+            const uint32_t V = W / 32;  // 2, 4 or 8 values per lane
+            if (t == NT_RATE1) {
+                uint32_t m = 0x7f800000u;
+                for (uint32_t q = 0; q < V; q++) m = min(m, __float_as_uint(nd[32 * q + lane]) & 0x7fffffffu);
+                m = __reduce_min_sync(FULL, m);
+                if (rate1_guard(__uint_as_float(m), ilog2(W))) {
+                    for (uint32_t q = 0; q < V; q++) {
+                        const uint32_t bits = __ballot_sync(FULL, nd[32 * q + lane] < 0.0f);
+                        if (lane == 0) xs[(pos >> 5) + q] = bits;
+                    }
+                    __syncwarp();
+                    entering = false;
+                    continue;
+                }
+            }
+            if (t == NT_REP) {
+                // SC's g-chain with zero partial sums, in SC's pairing order
+                float sm8[8];
 #pragma unroll
-    for (int q = 0; q < V; q++) v.x[q] = chan ? chan_load(p, fc, 32 * q + lane) : src[32 * q + lane];
-    uint32_t out[V];
-    if constexpr (V == 1) {
-        out[0] = engine32<FM>(v.x[0], lh, 32, wc);
-    } else {
-        const VecU<V> r = wlevel<FM, V>(v, lh, wc);
+                for (int q = 0; q < 8; q++) sm8[q] = q < (int)V ? nd[32 * q + lane] : 0.0f;
+                for (uint32_t hv = V / 2; hv >= 1; hv >>= 1)
 #pragma unroll
-        for (int q = 0; q < V; q++) out[q] = r.x[q];
-    }
-    if (lane < V) {
-        uint32_t o = out[0];
+                    for (int q = 0; q < 4; q++)
+                        if (q < (int)hv) sm8[q] = sm8[q + hv] + sm8[q];
+                float s0 = sm8[0];
+                for (int hh = 16; hh >= 1; hh >>= 1) {
+                    const float other = __shfl_down_sync(FULL, s0, hh);
+                    s0 = other + s0;
+                }
+                const uint32_t bits = __shfl_sync(FULL, s0, 0) < 0.0f ? FULL : 0u;
+                for (uint32_t w = lane; w < V; w += 32) xs[(pos >> 5) + w] = bits;
+                __syncwarp();
+                entering = false;
+                continue;
+            }
+            // mixed: f-step into the left child unless it is rate-0
+            const uint32_t H = W / 2, Vh = V / 2;
+            const uint8_t tl = plain ? NT_MIXED : ty[2 * lh];
+            if (tl == NT_RATE0) {
+                for (uint32_t w = lane; w < Vh; w += 32) xs[(pos >> 5) + w] = 0;
+                __syncwarp();
+                d++;
+                j = 2 * j;
+                entering = false;
+                continue;
+            }
+            float *ch = st_end - W;
+            float a[4], b[4];
 #pragma unroll
-        for (int q = 1; q < V; q++) o = lane == q ? out[q] : o;
-        xs[(pos >> 5) + lane] = o;
+            for (int q = 0; q < 4; q++)
+                if (q < (int)Vh) {
+                    a[q] = nd[32 * q + lane];
+                    b[q] = nd[32 * q + lane + H];
+                }
+#pragma unroll
+            for (int q = 0; q < 4; q++)
+                if (q < (int)Vh) {
+                    const float v = pq_f<FM>(a[q], b[q]);
+                    ch[32 * q + lane] = v;
+                    if (dump) dump[(size_t)(d + 1) * N + (size_t)(2 * j) * H + 32 * q + lane] = v;
+                }
+            __syncwarp();
+            d++;
+            j = 2 * j;
+            continue;
+        }
+        // ---- node (d, j) decided
+        if (d == d0) return;
+        if ((j & 1u) == 0) {
+            const uint8_t tr = plain ? NT_MIXED : ty[lh + 1];
+            const uint32_t posr = ((j + 1) * W) & (S - 1);
+            if (tr == NT_RATE0) {
+                for (uint32_t w = lane; w < W / 32; w += 32) xs[(posr >> 5) + w] = 0;
+                __syncwarp();
+                j++;
+                continue;
+            }
+            const float *par = st_end - 4 * W;
+            const uint32_t V = W / 32;
+            float a[4], b[4];
+            uint32_t sw[4];
+#pragma unroll
+            for (int q = 0; q < 4; q++)
+                if (q < (int)V) {
+                    a[q] = par[32 * q + lane];
+                    b[q] = par[32 * q + lane + W];
+                    sw[q] = xs[(pos >> 5) + q];
+                }
+#pragma unroll
+            for (int q = 0; q < 4; q++)
+                if (q < (int)V) {
+                    const float v = pq_g(a[q], b[q], (sw[q] >> lane) & 1u);
+                    nd[32 * q + lane] = v;
+                    if (dump) dump[(size_t)d * N + (size_t)(j + 1) * W + 32 * q + lane] = v;
+                }
+            __syncwarp();
+            j++;
+            entering = true;
+            continue;
+        }
+        for (uint32_t w = lane; w < W / 32; w += 32) xs[((pos - W) >> 5) + w] ^= xs[(pos >> 5) + w];
+        __syncwarp();
+        d--;
+        j >>= 1;
     }
 }
 
@@ -839,6 +832,17 @@ __global__ void __launch_bounds__(256, 2) sc_decode_kernel(DecParams p)
 
     const int tid = threadIdx.x, nthr = blockDim.x;
     const int dS = p.n - p.log2S;  // depth of the shared-memory sub-tree roots
+    // The narrow sub-trees are decoded by one warp.  Co-resident CTAs pick
+    // different warps so that their serial work lands on different SM
+    // sub-partitions (scheduler = hardware warp slot mod 4).
+    __shared__ int lw_sh;
+    if (tid == 0) {
+        uint32_t ws;
+        asm volatile("mov.u32 %0, %%warpid;" : "=r"(ws));
+        lw_sh = (int)((ws >> 3) & 3u);
+    }
+    __syncthreads();
+    const int lw = lw_sh;
     const uint32_t WMAX = S < 256 ? S : 256;  // nodes this wide or narrower: one warp, registers
 
     __shared__ unsigned long long eng_prof[4];
@@ -919,18 +923,21 @@ __global__ void __launch_bounds__(256, 2) sc_decode_kernel(DecParams p)
                 PROF_MARK(PR_WARP);
                 if (prof) pr_acc[PR_NODES_WARP]++;
                 __syncthreads();
-                if (tid < 32) {
+                if ((tid >> 5) == lw) {
                     const bool chan = d == 0;
-                    const float *src = chan ? nullptr : stage_ptr(p, fc, sm, W);
                     const int e = d - dS;
                     const uint32_t lh = (1u << e) + (j & ((1u << e) - 1u));
                     const uint32_t pos = (j * W) & (S - 1);
-                    switch (W) {
-                    case 256: warp_node<FM, 8>(src, chan, p, fc, lh, wc, sm.xs, pos); break;
-                    case 128: warp_node<FM, 4>(src, chan, p, fc, lh, wc, sm.xs, pos); break;
-                    case 64: warp_node<FM, 2>(src, chan, p, fc, lh, wc, sm.xs, pos); break;
-                    case 32: warp_node<FM, 1>(src, chan, p, fc, lh, wc, sm.xs, pos); break;
-                    default: warp_small<FM>(src, chan, p, fc, lh, wc, sm.xs, pos, (int)W); break;
+                    if (W >= 32) {
+                        if (chan) {  // whole block <= 256: stage the channel LLRs once
+                            float *dst = stage_ptr(p, fc, sm, W);
+                            for (uint32_t i = tid & 31; i < W; i += 32) dst[i] = chan_load(p, fc, i);
+                            __syncwarp();
+                        }
+                        warp_walk<FM>(sm.st + 2 * S, sm.xs, sm.ty, fc.dump, N, S, dS, wc.jS, p.plain, d, j);
+                    } else {
+                        const float *src = chan ? nullptr : stage_ptr(p, fc, sm, W);
+                        warp_small<FM>(src, chan, p, fc, lh, wc, sm.xs, pos, (int)W);
                     }
                 }
                 entering = false;
@@ -976,33 +983,20 @@ __global__ void __launch_bounds__(256, 2) sc_decode_kernel(DecParams p)
             }
             float *dst = stage_ptr(p, fc, sm, H);
             float *dmp = fc.dump ? fc.dump + (size_t)(d + 1) * N + (size_t)(2 * j) * H : nullptr;
-            // f-step, 4 consecutive elements per thread and 2 float4 chunks in flight
-            // (H >= 256 here, so every chunk is a whole float4)
+            // f-step, 4 consecutive elements per thread (H >= 256 here, so every
+            // chunk is a whole float4); the f's arithmetic hides the load latency
             const bool ch0 = d == 0;
 #pragma unroll 1
-            for (uint32_t base = 0; base < H; base += 8 * nthr) {
-                float4 a[2], b[2];
-#pragma unroll
-                for (int k = 0; k < 2; k++) {
-                    const uint32_t i = base + 4 * (tid + k * nthr);
-                    if (i < H) {
-                        a[k] = ch0 ? chan_load4(p, fc, i) : *reinterpret_cast<const float4 *>(src + i);
-                        b[k] = ch0 ? chan_load4(p, fc, i + H) : *reinterpret_cast<const float4 *>(src + i + H);
-                    }
-                }
-#pragma unroll
-                for (int k = 0; k < 2; k++) {
-                    const uint32_t i = base + 4 * (tid + k * nthr);
-                    if (i < H) {
-                        float4 v;
-                        v.x = pq_f<FM>(a[k].x, b[k].x);
-                        v.y = pq_f<FM>(a[k].y, b[k].y);
-                        v.z = pq_f<FM>(a[k].z, b[k].z);
-                        v.w = pq_f<FM>(a[k].w, b[k].w);
-                        *reinterpret_cast<float4 *>(dst + i) = v;
-                        if (dmp) *reinterpret_cast<float4 *>(dmp + i) = v;
-                    }
-                }
+            for (uint32_t i = 4 * tid; i < H; i += 4 * nthr) {
+                const float4 a = ch0 ? chan_load4(p, fc, i) : *reinterpret_cast<const float4 *>(src + i);
+                const float4 b = ch0 ? chan_load4(p, fc, i + H) : *reinterpret_cast<const float4 *>(src + i + H);
+                float4 v;
+                v.x = pq_f<FM>(a.x, b.x);
+                v.y = pq_f<FM>(a.y, b.y);
+                v.z = pq_f<FM>(a.z, b.z);
+                v.w = pq_f<FM>(a.w, b.w);
+                *reinterpret_cast<float4 *>(dst + i) = v;
+                if (dmp) *reinterpret_cast<float4 *>(dmp + i) = v;
             }
             d++;
             j = 2 * j;

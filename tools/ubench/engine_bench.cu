@@ -18,6 +18,28 @@ __global__ void k_f_latency(const float *in, float *out, int iters, long long *c
     if (threadIdx.x == 0) cyc[0] = t1 - t0;
 }
 
+template <int ILP>
+__global__ void k_f_ilp(const float *in, float *out, int iters, long long *cyc)
+{
+    load_log_table();
+    __syncthreads();
+    float a[ILP], b = in[threadIdx.x + 32];
+#pragma unroll
+    for (int k = 0; k < ILP; k++) a[k] = in[(threadIdx.x + k) & 31];
+    long long t0 = clock64();
+    for (int i = 0; i < iters; i++) {
+#pragma unroll
+        for (int k = 0; k < ILP; k++) a[k] = pq_f<PQ_F_EXACT>(a[k], b) + 0.5f;
+        b = b * 1.0001f;
+    }
+    long long t1 = clock64();
+    float s = 0;
+#pragma unroll
+    for (int k = 0; k < ILP; k++) s += a[k];
+    out[threadIdx.x] = s;
+    if (threadIdx.x == 0) cyc[0] = t1 - t0;
+}
+
 __global__ void k_shfl_latency(const float *in, float *out, int iters, long long *cyc)
 {
     float a = in[threadIdx.x];
@@ -101,6 +123,15 @@ int main()
     for (int r = 0; r < 2; r++) k_f_latency<<<1, 32>>>(in, out, iters, cyc);
     cudaMemcpy(&c, cyc, 8, cudaMemcpyDeviceToHost);
     printf("f latency: %.1f cycles\n", (double)c / iters);
+    for (int r = 0; r < 2; r++) k_f_ilp<2><<<1, 32>>>(in, out, iters, cyc);
+    cudaMemcpy(&c, cyc, 8, cudaMemcpyDeviceToHost);
+    printf("f x2 ILP: %.1f cycles per iteration\n", (double)c / iters);
+    for (int r = 0; r < 2; r++) k_f_ilp<4><<<1, 32>>>(in, out, iters, cyc);
+    cudaMemcpy(&c, cyc, 8, cudaMemcpyDeviceToHost);
+    printf("f x4 ILP: %.1f cycles per iteration\n", (double)c / iters);
+    for (int r = 0; r < 2; r++) k_f_ilp<8><<<1, 32>>>(in, out, iters, cyc);
+    cudaMemcpy(&c, cyc, 8, cudaMemcpyDeviceToHost);
+    printf("f x8 ILP: %.1f cycles per iteration\n", (double)c / iters);
     for (int r = 0; r < 2; r++) k_shfl_latency<<<1, 32>>>(in, out, iters, cyc);
     cudaMemcpy(&c, cyc, 8, cudaMemcpyDeviceToHost);
     printf("shfl+add latency: %.1f cycles\n", (double)c / iters);
