@@ -80,43 +80,95 @@ static inline double f_f64(double a, double b, int fmode)
 }
 
 /* ------------------------------------------------------------------------- */
-/* fp32 mirror of the GPU's exact boxplus: the same tables and the same
- * IEEE-only operation sequence (add, mul, fma, floor), so the GPU must
- * reproduce it bit for bit.
- *   lo >= 1:  |f| = (lo - C(hi - lo)) + C(hi + lo),  C(x) = log1p(e^-x)
- *   lo <  1:  |f| = y A(y),  y = T(lo) T(hi),  T(x) = x G(x) = tanh(x/2),
- *             A(y) = 2 atanh(y) / y
- * C, G: piecewise cubics on [0, 24) (1/8 intervals); A on [0, 1/2) (1/64);
- * C(x >= 24) = 0, T(x >= 24) = 1.  Tables: tools/gen_fmag_tables.py.      */
+/* fp32 mirror of the GPU's exact boxplus: the same IEEE-only operation
+ * sequence (add, mul, fma, rint, integer bit operations; no division), so
+ * the GPU must reproduce it bit for bit.
+ *   |f| = log1p((1-e^-lo)(1-e^-hi) / (e^-lo + e^-hi))   lo <= 8
+ *       = lo - log1p(e^-(hi-lo))                       lo >  8
+ * expm:  Cody-Waite reduction + Taylor-7 expm1, x clamped at 86.5
+ * rcp:   integer seed + three Newton steps
+ * log1p: Fast2Sum of 1+q, 32-entry table of 1/T_j, log T_j (T_j = 1 + j/32),
+ *        degree-6 log1p of the reduced argument                            */
 
 static inline float u2f(uint32_t u) { float f; memcpy(&f, &u, 4); return f; }
 static inline uint32_t f2u(float f) { uint32_t u; memcpy(&u, &f, 4); return u; }
 
-#include "fmag_tables.inc"
+#define M_LN2_HI 0.693145751953125f
+#define M_LN2_LO 1.42860682030941723212e-6f
+#define M_INV_LN2 1.44269504088896341f
 
-static inline float tab_eval(const uint32_t *tab, float xs, int kmax)
+static const uint32_t LOG_TAB[64] = {
+    0x3f800000u, 0x3f783e10u, 0x3f70f0f1u, 0x3f6a0ea1u, 0x3f638e39u, 0x3f5d67c9u, 0x3f579436u, 0x3f520d21u,
+    0x3f4ccccdu, 0x3f47ce0cu, 0x3f430c31u, 0x3f3e82fau, 0x3f3a2e8cu, 0x3f360b61u, 0x3f321643u, 0x3f2e4c41u,
+    0x3f2aaaabu, 0x3f272f05u, 0x3f23d70au, 0x3f20a0a1u, 0x3f1d89d9u, 0x3f1a90e8u, 0x3f17b426u, 0x3f14f209u,
+    0x3f124925u, 0x3f0fb824u, 0x3f0d3dcbu, 0x3f0ad8f3u, 0x3f088889u, 0x3f064b8au, 0x3f042108u, 0x3f020821u,
+    0x00000000u, 0x3cfc14d8u, 0x3d785186u, 0x3db78694u, 0x3df1383bu, 0x3e14aa98u, 0x3e2ff984u, 0x3e4a92d5u,
+    0x3e647fbeu, 0x3e7dc8c3u, 0x3e8b3ae5u, 0x3e974716u, 0x3ea30c5eu, 0x3eae8deeu, 0x3eb9cec0u, 0x3ec4d19cu,
+    0x3ecf991fu, 0x3eda27bcu, 0x3ee47fbeu, 0x3eeea350u, 0x3ef8947bu, 0x3f012a95u, 0x3f05f397u, 0x3f0aa61fu,
+    0x3f0f42fbu, 0x3f13caf1u, 0x3f183ebau, 0x3f1c9f07u, 0x3f20ec7fu, 0x3f2527c3u, 0x3f295169u, 0x3f2d6a02u};
+
+static inline void expm_f32(float x, float *e, float *m)
 {
-    float kf = floorf(xs);
-    int k = (int)kf;
-    if (k > kmax) k = kmax;
-    float u = xs - (float)k;
-    const uint32_t *c = tab + 4 * k;
-    return fmaf(fmaf(fmaf(u2f(c[3]), u, u2f(c[2])), u, u2f(c[1])), u, u2f(c[0]));
+    x = fminf(x, 86.5f);
+    float kf = rintf(x * M_INV_LN2);
+    float r = fmaf(-kf, M_LN2_HI, x);
+    r = fmaf(-kf, M_LN2_LO, r);
+    float t = -r;
+    float h = fmaf(t, 1.0f / 40320.0f, 1.0f / 5040.0f);
+    h = fmaf(t, h, 1.0f / 720.0f);
+    h = fmaf(t, h, 1.0f / 120.0f);
+    h = fmaf(t, h, 1.0f / 24.0f);
+    h = fmaf(t, h, 1.0f / 6.0f);
+    h = fmaf(t, h, 0.5f);
+    float p = fmaf(t * t, h, t);
+    float s = u2f((uint32_t)(127 - (int)kf) << 23);
+    *e = fmaf(s, p, s);
+    *m = fmaf(-s, p, 1.0f - s);
+}
+
+static inline float rcp_f32(float d)
+{
+    float r = u2f(0x7ef311c7u - f2u(d));
+    float e = fmaf(-d, r, 1.0f);
+    r = fmaf(r, e, r);
+    e = fmaf(-d, r, 1.0f);
+    r = fmaf(r, e, r);
+    e = fmaf(-d, r, 1.0f);
+    return fmaf(r, e, r);
+}
+
+static inline float log1p_f32(float q)
+{
+    float u = 1.0f + q;
+    float err = (fmaxf(1.0f, q) - u) + fminf(1.0f, q);
+    uint32_t b = f2u(u);
+    int k = (int)(b >> 23) - 127;
+    uint32_t j = (b >> 18) & 31u;
+    float m = u2f((b & 0x007fffffu) | 0x3f800000u);
+    float T = u2f(0x3f800000u | (j << 18));
+    float invT = u2f(LOG_TAB[j]), logT = u2f(LOG_TAB[32 + j]);
+    float r = (m - T) * invT;
+    float p = fmaf(r, -1.0f / 6.0f, 0.2f);
+    p = fmaf(r, p, -0.25f);
+    p = fmaf(r, p, 1.0f / 3.0f);
+    p = fmaf(r, p, -0.5f);
+    p = fmaf(r, p, 1.0f);
+    p = p * r;
+    float inv_u = u2f((uint32_t)(127 - k) << 23) * invT;
+    float kf = (float)k;
+    return fmaf(kf, M_LN2_HI, fmaf(kf, M_LN2_LO, logT + (p + err * inv_u)));
 }
 
 float orc_fmag_f32(float a, float b)
 {
     float lo = fminf(a, b), hi = fmaxf(a, b);
-    if (lo >= 1.0f) {
-        float dd = hi - lo, ss = hi + lo;
-        float cd = dd < 24.0f ? tab_eval(FMAG_TAB_C, dd * 8.0f, 191) : 0.0f;
-        float cs = ss < 24.0f ? tab_eval(FMAG_TAB_C, ss * 8.0f, 191) : 0.0f;
-        return (lo - cd) + cs;
-    }
-    float tl = lo * tab_eval(FMAG_TAB_G, lo * 8.0f, 191);
-    float th = hi < 24.0f ? hi * tab_eval(FMAG_TAB_G, hi * 8.0f, 191) : 1.0f;
-    float y = tl * th;
-    return y * tab_eval(FMAG_TAB_A, y * 64.0f, 31);
+    int big = lo > 8.0f;
+    float e1, m1, e2, m2;
+    expm_f32(big ? hi - lo : lo, &e1, &m1);
+    expm_f32(hi, &e2, &m2);
+    float q = (m1 * m2) * rcp_f32(e1 + e2);
+    float l = log1p_f32(big ? e1 : q);
+    return big ? lo - l : l;
 }
 
 static inline float f_f32(float a, float b, int fmode)

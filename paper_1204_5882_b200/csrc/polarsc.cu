@@ -70,64 +70,109 @@ static int set_err(int code, const char *fmt, ...)
     } while (0)
 
 // ---------------------------------------------------------------------------
-// device math: the exact boxplus, table-driven, IEEE-only fp32 (add, mul,
-// fma, floor and integer ops; no MUFU, no division).  The fp32 oracle
-// mirror (oracle/sc_oracle.c:orc_fmag_f32) evaluates the same tables with
-// the same operation sequence; the two agree bit for bit
-// (tests/test_gpu_parity.py compares every stage LLR).
-//
-//   lo >= 1:  |f| = (lo - C(hi - lo)) + C(hi + lo),  C(x) = log1p(e^-x)
-//             -- the reference's stable boxplus, construction.py:300-303;
-//             here every term is O(1) and |f| >= 0.43, so no cancellation
-//   lo <  1:  |f| = y A(y),  y = T(lo) T(hi),  T(x) = tanh(x/2) = x G(x),
-//             A(y) = 2 atanh(y)/y  -- the phi-form phi(phi(a) + phi(b))
-//              written without cancellation for small inputs
-// C, G on [0, 24) and A on [0, 1/2) are piecewise cubics (192, 192 and 32
-// intervals; tools/gen_fmag_tables.py); C(x >= 24) = 0 (< 4e-11) and
-// T(x >= 24) = 1.  Max relative error vs f64 ~4e-7.
+// device math: the exact boxplus in branch-free, IEEE-only fp32 (add, mul,
+// fma, rint and integer bit operations -- no MUFU, no division).  Mirrored
+// operation for operation by oracle/sc_oracle.c:orc_fmag_f32; the two must
+// agree bit for bit (tests/test_gpu_parity.py checks every stage LLR).
 
-#include "fmag_tables.inc"
+#define LN2_HI 0.693145751953125f
+#define LN2_LO 1.42860682030941723212e-6f
+#define INV_LN2 1.44269504088896341f
 
-// staged into shared memory at kernel start: lanes index the tables with
-// divergent interval numbers, which shared memory serves far better than
-// the constant cache
-__shared__ float4 pq_ftab[416];
+// 1/T_j and log(T_j), T_j = 1 + j/32, rounded to fp32 (same bits in the oracle)
+__constant__ uint32_t c_log_tab[64] = {
+    0x3f800000u, 0x3f783e10u, 0x3f70f0f1u, 0x3f6a0ea1u, 0x3f638e39u, 0x3f5d67c9u, 0x3f579436u, 0x3f520d21u,
+    0x3f4ccccdu, 0x3f47ce0cu, 0x3f430c31u, 0x3f3e82fau, 0x3f3a2e8cu, 0x3f360b61u, 0x3f321643u, 0x3f2e4c41u,
+    0x3f2aaaabu, 0x3f272f05u, 0x3f23d70au, 0x3f20a0a1u, 0x3f1d89d9u, 0x3f1a90e8u, 0x3f17b426u, 0x3f14f209u,
+    0x3f124925u, 0x3f0fb824u, 0x3f0d3dcbu, 0x3f0ad8f3u, 0x3f088889u, 0x3f064b8au, 0x3f042108u, 0x3f020821u,
+    0x00000000u, 0x3cfc14d8u, 0x3d785186u, 0x3db78694u, 0x3df1383bu, 0x3e14aa98u, 0x3e2ff984u, 0x3e4a92d5u,
+    0x3e647fbeu, 0x3e7dc8c3u, 0x3e8b3ae5u, 0x3e974716u, 0x3ea30c5eu, 0x3eae8deeu, 0x3eb9cec0u, 0x3ec4d19cu,
+    0x3ecf991fu, 0x3eda27bcu, 0x3ee47fbeu, 0x3eeea350u, 0x3ef8947bu, 0x3f012a95u, 0x3f05f397u, 0x3f0aa61fu,
+    0x3f0f42fbu, 0x3f13caf1u, 0x3f183ebau, 0x3f1c9f07u, 0x3f20ec7fu, 0x3f2527c3u, 0x3f295169u, 0x3f2d6a02u};
+// staged into shared memory at kernel start: lanes index it with divergent j,
+// which shared memory serves without bank conflicts (32 distinct words)
+__shared__ float pq_tab[64];
 
-__device__ __forceinline__ void load_fmag_tables()
+__device__ __forceinline__ void load_log_table()
 {
-    const uint4 *c = reinterpret_cast<const uint4 *>(FMAG_TAB_C);
-    const uint4 *g = reinterpret_cast<const uint4 *>(FMAG_TAB_G);
-    const uint4 *a = reinterpret_cast<const uint4 *>(FMAG_TAB_A);
-    for (int i = threadIdx.x; i < 416; i += blockDim.x) {
-        const uint4 v = i < 192 ? c[i] : (i < 384 ? g[i - 192] : a[i - 384]);
-        pq_ftab[i] = make_float4(__uint_as_float(v.x), __uint_as_float(v.y), __uint_as_float(v.z),
-                                 __uint_as_float(v.w));
-    }
+    for (int i = threadIdx.x; i < 64; i += blockDim.x) pq_tab[i] = __uint_as_float(c_log_tab[i]);
 }
 
-// cubic of interval floor(xs) (clamped to kmax) at u = xs - k
-__device__ __forceinline__ float tab_eval(const float4 *tab, float xs, int kmax)
+// e = e^-x, m = 1 - e^-x for x >= 0 (x clamped at 86.5: e stays a normal
+// float; beyond that e^-x < 2.3e-38 never changes a result).
+// Cody-Waite reduction x = k ln2 + r, |r| <= ln2/2; Taylor-7 expm1(-r).
+__device__ __forceinline__ void pq_expm(float x, float &e, float &m)
 {
-    const float kf = floorf(xs);
-    const int k = min((int)kf, kmax);
-    const float u = xs - (float)k;
-    const float4 c = tab[k];
-    return fmaf(fmaf(fmaf(c.w, u, c.z), u, c.y), u, c.x);
+    x = fminf(x, 86.5f);
+    const float kf = rintf(x * INV_LN2);
+    float r = fmaf(-kf, LN2_HI, x);
+    r = fmaf(-kf, LN2_LO, r);
+    const float t = -r;
+    float h = fmaf(t, 1.0f / 40320.0f, 1.0f / 5040.0f);
+    h = fmaf(t, h, 1.0f / 720.0f);
+    h = fmaf(t, h, 1.0f / 120.0f);
+    h = fmaf(t, h, 1.0f / 24.0f);
+    h = fmaf(t, h, 1.0f / 6.0f);
+    h = fmaf(t, h, 0.5f);
+    const float p = fmaf(t * t, h, t);
+    const float s = __uint_as_float((uint32_t)(127 - (int)kf) << 23);  // 2^-k
+    e = fmaf(s, p, s);
+    m = fmaf(-s, p, 1.0f - s);
 }
 
+// 1/d for d in [2^-126, 2]: integer seed, three Newton steps (FMA only)
+__device__ __forceinline__ float pq_rcp(float d)
+{
+    float r = __uint_as_float(0x7ef311c7u - __float_as_uint(d));
+    float e = fmaf(-d, r, 1.0f);
+    r = fmaf(r, e, r);
+    e = fmaf(-d, r, 1.0f);
+    r = fmaf(r, e, r);
+    e = fmaf(-d, r, 1.0f);
+    return fmaf(r, e, r);
+}
+
+// log1p(q), 0 <= q < 2^100: u = 1 + q with its exact rounding error (Fast2Sum),
+// u = 2^k m, m in [T_j, T_j + 1/32), log m = log T_j + log1p((m - T_j)/T_j)
+__device__ __forceinline__ float pq_log1p(float q)
+{
+    const float u = 1.0f + q;
+    const float err = (fmaxf(1.0f, q) - u) + fminf(1.0f, q);
+    const uint32_t b = __float_as_uint(u);
+    const int k = (int)(b >> 23) - 127;
+    const uint32_t j = (b >> 18) & 31u;
+    const float m = __uint_as_float((b & 0x007fffffu) | 0x3f800000u);
+    const float T = __uint_as_float(0x3f800000u | (j << 18));
+    const float invT = pq_tab[j], logT = pq_tab[32 + j];
+    const float r = (m - T) * invT;
+    float p = fmaf(r, -1.0f / 6.0f, 0.2f);
+    p = fmaf(r, p, -0.25f);
+    p = fmaf(r, p, 1.0f / 3.0f);
+    p = fmaf(r, p, -0.5f);
+    p = fmaf(r, p, 1.0f);
+    p = p * r;
+    const float inv_u = __uint_as_float((uint32_t)(127 - k) << 23) * invT;
+    const float kf = (float)k;
+    return fmaf(kf, LN2_HI, fmaf(kf, LN2_LO, logT + (p + err * inv_u)));
+}
+
+// |f| for magnitudes a, b >= 0 (lo = min, hi = max):
+//   lo <= 8:  log1p((1 - e^-lo)(1 - e^-hi) / (e^-lo + e^-hi))
+//   lo >  8:  lo - log1p(e^-(hi - lo))      (drops log1p(e^-(lo+hi)) < 1.2e-7, i.e.
+//                                            < 2e-8 relative to a result >= 7.3)
+// = log((1 + e^-a e^-b)/(e^-a + e^-b)) = phi(phi(a) + phi(b)),
+// the reference's stable boxplus (construction.py:300-303) in a form free of
+// its cancellation at small magnitudes.  Max relative error ~3.4e-7.
 __device__ __forceinline__ float pq_fmag(float a, float b)
 {
     const float lo = fminf(a, b), hi = fmaxf(a, b);
-    if (lo >= 1.0f) {
-        const float dd = hi - lo, ss = hi + lo;
-        const float cd = dd < 24.0f ? tab_eval(pq_ftab, dd * 8.0f, 191) : 0.0f;
-        const float cs = ss < 24.0f ? tab_eval(pq_ftab, ss * 8.0f, 191) : 0.0f;
-        return (lo - cd) + cs;
-    }
-    const float tl = lo * tab_eval(pq_ftab + 192, lo * 8.0f, 191);
-    const float th = hi < 24.0f ? hi * tab_eval(pq_ftab + 192, hi * 8.0f, 191) : 1.0f;
-    const float y = tl * th;
-    return y * tab_eval(pq_ftab + 384, y * 64.0f, 31);
+    const bool big = lo > 8.0f;
+    float e1, m1, e2, m2;
+    pq_expm(big ? hi - lo : lo, e1, m1);
+    pq_expm(hi, e2, m2);
+    const float q = (m1 * m2) * pq_rcp(e1 + e2);
+    const float l = pq_log1p(big ? e1 : q);
+    return big ? lo - l : l;
 }
 
 template <int FM>
@@ -774,7 +819,7 @@ __global__ void __launch_bounds__(256, 2) sc_decode_kernel(DecParams p)
     const uint32_t SW = S >= 32 ? S / 32 : 1;
     sm.ty = (uint8_t *)(sm.xs + SW);
 
-    load_fmag_tables();
+    load_log_table();
     __syncthreads();
     const uint32_t frame = blockIdx.x;
     FrameCtx fc;

@@ -5,7 +5,7 @@
 
 __global__ void k_f_latency(const float *in, float *out, int iters, long long *cyc)
 {
-    load_fmag_tables();
+    load_log_table();
     __syncthreads();
     float a = in[threadIdx.x], b = in[threadIdx.x + 32];
     long long t0 = clock64();
@@ -21,7 +21,7 @@ __global__ void k_f_latency(const float *in, float *out, int iters, long long *c
 template <int ILP>
 __global__ void k_f_ilp(const float *in, float *out, int iters, long long *cyc)
 {
-    load_fmag_tables();
+    load_log_table();
     __syncthreads();
     float a[ILP], b = in[threadIdx.x + 32];
 #pragma unroll
@@ -54,7 +54,7 @@ __global__ void k_shfl_latency(const float *in, float *out, int iters, long long
 __global__ void k_engine(const float *in, const uint8_t *ty_g, float *out, int iters, int plain, long long *cyc)
 {
     __shared__ uint8_t ty[64];
-    load_fmag_tables();
+    load_log_table();
     for (int i = threadIdx.x; i < 64; i += 32) ty[i] = ty_g[i];
     __syncthreads();
     WarpCtx c;
@@ -84,7 +84,7 @@ __global__ void k_c1_warp(const uint8_t *types_g, const float *llr, long long *c
     __shared__ uint8_t ty[2048];
     __shared__ float st[2048];
     __shared__ uint32_t xs[32];
-    load_fmag_tables();
+    load_log_table();
     for (int i = threadIdx.x; i < 2048; i += 32) ty[i] = types_g[i];
     __syncthreads();
     const int lane = threadIdx.x & 31;
