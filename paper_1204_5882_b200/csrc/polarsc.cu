@@ -186,18 +186,25 @@ __device__ __forceinline__ float pq_f(float a, float b)
 // g(a, b, s) = b + (1 - 2s) a
 __device__ __forceinline__ float pq_g(float a, float b, uint32_t s) { return s ? b - a : b + a; }
 
-// Lower bound on |boxplus(t, t)| (exact arithmetic): 0.427 t^2 for t < 1,
-// max(0.427, t - ln 2) for t >= 1.  Chained k times from min|L| of a rate-1
-// node it lower-bounds every LLR inside the node's sub-tree (|g| >= max of its
-// operands there, boxplus is monotone), so a result >= 1e-30 proves no fp32
-// underflow to an exact zero -- the only way plain SC could decide differently
-// from the node's hard decisions.  tests/test_oracle.py checks the bound.
-__device__ __forceinline__ bool rate1_guard(float m, int k)
-{
-    float t = m;
-    for (int i = 0; i < k; i++) t = t < 1.0f ? 0.427f * t * t : fmaxf(0.427f, t - 0.6932f);
-    return t >= 1e-30f;
-}
+// Rate-1 shortcut guard.  b(t) = 0.427 t^2 (t < 1), max(0.427, t - ln 2)
+// (t >= 1) lower-bounds |boxplus(t, t)| in exact arithmetic; chained k times
+// from m = min|L| of a rate-1 node of width 2^k it lower-bounds every LLR
+// inside the node's sub-tree (|g| >= max of its operands there -- the signs
+// agree by construction -- and boxplus is monotone).  A chain result >= 1e-30
+// proves no fp32 underflow to an exact zero can occur, the only way plain SC
+// could decide differently from the node's hard decisions.  RATE1_TAU[k] is
+// the smallest fp32 m (rounded up, plus one ulp) whose chain reaches 1e-30;
+// tests/test_oracle.py re-derives the table and checks b(t) <= |f(t, t)|.
+__constant__ float RATE1_TAU[26] = {
+    1.000000097210625e-30f, 1.5303335787713972e-15f, 5.986585449591075e-08f, 0.00037443434121087193f,
+    0.02961242012679577f, 0.26334378123283386f, 0.7853217124938965f, 1.4785218238830566f,
+    2.171721935272217f, 2.864922046661377f, 3.558121919631958f, 4.251322269439697f,
+    4.944522380828857f, 5.637722492218018f, 6.3309221267700195f, 7.02412223815918f,
+    7.71732234954834f, 8.410523414611816f, 9.103723526000977f, 9.79692268371582f,
+    10.49012279510498f, 11.18332290649414f, 11.8765230178833f, 12.569723129272461f,
+    13.262923240661621f, 13.956123352050781f};
+
+__device__ __forceinline__ bool rate1_guard(float m, int k) { return m >= RATE1_TAU[k]; }
 
 // ---------------------------------------------------------------------------
 // node types (host computes them from the frozen mask; heap order)
@@ -375,7 +382,7 @@ __device__ __forceinline__ uint32_t dec2(float a, float b, const TypeBits &T, in
     const uint32_t t = plain ? NT_MIXED : tget(T, h);
     if (t == NT_RATE0) return 0u;
     if (t == NT_REP) return (b + a) < 0.0f ? 3u : 0u;
-    if (t == NT_RATE1 && rate1_guard(fminf(fabsf(a), fabsf(b)), 1))
+    if (t == NT_RATE1 && fminf(fabsf(a), fabsf(b)) >= 1.5303335787713972e-15f)  // RATE1_TAU[1]
         return (a < 0.0f ? 1u : 0u) | (b < 0.0f ? 2u : 0u);
     const bool fa = (T.leaf >> (2 * h - 32)) & 1u, fb = (T.leaf >> (2 * h - 31)) & 1u;
     const float l = pq_f<FM>(a, b);
@@ -389,7 +396,40 @@ __device__ __forceinline__ uint32_t dec2(float a, float b, const TypeBits &T, in
     return (u0 ^ u1) | (u1 << 1);
 }
 
-// ---- lane-parallel levels: lane i holds element i of a W = 16 / 32 node
+// W = 4 node whose four values every lane holds: the whole sub-tree in
+// registers, no shuffles (uniform branches on the node types only).
+template <int FM>
+__device__ __forceinline__ uint32_t dec4(float x0, float x1, float x2, float x3, const TypeBits &T, int h,
+                                         bool plain, const NodePos &np)
+{
+    const uint32_t t = plain ? NT_MIXED : tget(T, h);
+    if (t == NT_RATE0) return 0u;
+    if (t == NT_REP) return ((x3 + x1) + (x2 + x0)) < 0.0f ? 15u : 0u;
+    if (t == NT_RATE1 &&
+        fminf(fminf(fabsf(x0), fabsf(x1)), fminf(fabsf(x2), fabsf(x3))) >= 5.986585449591075e-08f)  // TAU[2]
+        return (x0 < 0.0f ? 1u : 0u) | (x1 < 0.0f ? 2u : 0u) | (x2 < 0.0f ? 4u : 0u) | (x3 < 0.0f ? 8u : 0u);
+    uint32_t xl = 0, xr = 0;
+    const bool lane0 = (threadIdx.x & 31) == 0;
+    if (plain || tget(T, 2 * h) != NT_RATE0) {
+        const float c0 = pq_f<FM>(x0, x2), c1 = pq_f<FM>(x1, x3);
+        if (np.dump && lane0) {
+            np.dump[(size_t)(np.d + 1) * np.N + 4 * np.j] = c0;
+            np.dump[(size_t)(np.d + 1) * np.N + 4 * np.j + 1] = c1;
+        }
+        xl = dec2<FM>(c0, c1, T, 2 * h, plain, child_pos(np, 0));
+    }
+    if (plain || tget(T, 2 * h + 1) != NT_RATE0) {
+        const float c0 = pq_g(x0, x2, xl & 1u), c1 = pq_g(x1, x3, (xl >> 1) & 1u);
+        if (np.dump && lane0) {
+            np.dump[(size_t)(np.d + 1) * np.N + 4 * np.j + 2] = c0;
+            np.dump[(size_t)(np.d + 1) * np.N + 4 * np.j + 3] = c1;
+        }
+        xr = dec2<FM>(c0, c1, T, 2 * h + 1, plain, child_pos(np, 1));
+    }
+    return ((xl ^ xr) & 3u) | (xr << 2);
+}
+
+// ---- lane-parallel levels: lane i holds element i of a W = 8 / 16 / 32 node
 
 // rate-1 / repetition handling of a node held one element per lane (lanes < W)
 __device__ __forceinline__ bool lanes_special(float v, int W, uint32_t t, uint32_t &bits)
@@ -401,58 +441,37 @@ __device__ __forceinline__ bool lanes_special(float v, int W, uint32_t t, uint32
         return true;
     }
     if (t == NT_RATE1) {
-        uint32_t m = lane < W ? (__float_as_uint(v) & 0x7fffffffu) : 0x7f800000u;
-        m = __reduce_min_sync(FULL, m);
-        if (rate1_guard(__uint_as_float(m), ilog2((uint32_t)W))) {
-            bits = __ballot_sync(FULL, lane < W && v < 0.0f) & lowmask(W);
+        // both votes issue back to back: guard (all |L| >= tau) and the signs
+        const bool ok = __all_sync(FULL, lane >= W || fabsf(v) >= RATE1_TAU[ilog2((uint32_t)W)]);
+        const uint32_t neg = __ballot_sync(FULL, lane < W && v < 0.0f);
+        if (ok) {
+            bits = neg & lowmask(W);
             return true;
         }
     }
     if (t == NT_REP) {
-        float sum = v;
-        for (int hh = W / 2; hh >= 1; hh >>= 1) {
-            const float other = __shfl_down_sync(FULL, sum, hh);
-            sum = other + sum;
-        }
-        bits = __shfl_sync(FULL, sum, 0) < 0.0f ? lowmask(W) : 0u;
+        // all values to every lane, then SC's g-chain sum in its pairing order
+        float x[32];
+#pragma unroll
+        for (int i = 0; i < 32; i++) x[i] = i < W ? __shfl_sync(FULL, v, i) : 0.0f;
+#pragma unroll
+        for (int hh = 16; hh >= 1; hh >>= 1)
+            if (hh < W)
+#pragma unroll
+                for (int i = 0; i < hh; i++) x[i] = x[i + hh] + x[i];
+        bits = x[0] < 0.0f ? lowmask(W) : 0u;
         return true;
     }
     return false;
 }
 
-
-// W = 4 node, lane i holds element i (lanes 0..3): lane-parallel f/g, the two
-// width-2 children decided in closed form in every lane's registers.
-template <int FM>
-__device__ __forceinline__ uint32_t dec4(float v, const TypeBits &T, int h, bool plain, const NodePos &np)
-{
-    const unsigned FULL = 0xffffffffu;
-    uint32_t bits;
-    if (!plain && lanes_special(v, 4, tget(T, h), bits)) return bits;
-    const float b = __shfl_down_sync(FULL, v, 2);
-    uint32_t xl = 0, xr = 0;
-    if (plain || tget(T, 2 * h) != NT_RATE0) {
-        const float c = pq_f<FM>(v, b);
-        const float c0 = __shfl_sync(FULL, c, 0), c1 = __shfl_sync(FULL, c, 1);
-        dump_lanes(child_pos(np, 0), c, 2);
-        xl = dec2<FM>(c0, c1, T, 2 * h, plain, child_pos(np, 0));
-    }
-    if (plain || tget(T, 2 * h + 1) != NT_RATE0) {
-        const float c = pq_g(v, b, (xl >> ((threadIdx.x & 31) & 1)) & 1u);
-        const float c0 = __shfl_sync(FULL, c, 0), c1 = __shfl_sync(FULL, c, 1);
-        dump_lanes(child_pos(np, 1), c, 2);
-        xr = dec2<FM>(c0, c1, T, 2 * h + 1, plain, child_pos(np, 1));
-    }
-    return ((xl ^ xr) & 3u) | (xr << 2);
-}
-
-// W = 8 node, lane i holds element i (lanes 0..7).  One copy (noinline).
+// W = 8 node, lane i holds element i (lanes 0..7).  One copy (noinline):
+// lane-parallel f/g step, then the width-4 children in registers.
 template <int FM>
 __device__ __noinline__ uint32_t dec8(float v, const TypeBits T, int h, bool plain, const NodePos np)
 {
     UB_BEGIN();
     const unsigned FULL = 0xffffffffu;
-    const int lane = threadIdx.x & 31;
     uint32_t bits;
     if (!plain && lanes_special(v, 8, tget(T, h), bits)) {
         UB_END(0);
@@ -463,12 +482,14 @@ __device__ __noinline__ uint32_t dec8(float v, const TypeBits T, int h, bool pla
     if (plain || tget(T, 2 * h) != NT_RATE0) {
         const float c = pq_f<FM>(v, b);
         dump_lanes(child_pos(np, 0), c, 4);
-        xl = dec4<FM>(c, T, 2 * h, plain, child_pos(np, 0));
+        xl = dec4<FM>(__shfl_sync(FULL, c, 0), __shfl_sync(FULL, c, 1), __shfl_sync(FULL, c, 2),
+                      __shfl_sync(FULL, c, 3), T, 2 * h, plain, child_pos(np, 0));
     }
     if (plain || tget(T, 2 * h + 1) != NT_RATE0) {
-        const float c = pq_g(v, b, (xl >> (lane & 3)) & 1u);
+        const float c = pq_g(v, b, (xl >> ((threadIdx.x & 31) & 3)) & 1u);
         dump_lanes(child_pos(np, 1), c, 4);
-        xr = dec4<FM>(c, T, 2 * h + 1, plain, child_pos(np, 1));
+        xr = dec4<FM>(__shfl_sync(FULL, c, 0), __shfl_sync(FULL, c, 1), __shfl_sync(FULL, c, 2),
+                      __shfl_sync(FULL, c, 3), T, 2 * h + 1, plain, child_pos(np, 1));
     }
     UB_END(0);
     return (xl ^ xr) | (xr << 4);
@@ -562,10 +583,10 @@ __device__ __forceinline__ uint32_t engine32_body(float A, uint32_t root, int W0
     if (W0 == 32) return dec32<FM>(A, T, plain, np);
     if (W0 == 16) return dec16<FM>(A, T, 2, plain, np);
     if (W0 == 8) return dec8<FM>(A, T, 4, plain, np);
-    if (W0 == 4) return dec4<FM>(A, T, 8, plain, np);
     float x[4];
 #pragma unroll
-    for (int i = 0; i < 2; i++) x[i] = __shfl_sync(0xffffffffu, A, i);
+    for (int i = 0; i < 4; i++) x[i] = __shfl_sync(0xffffffffu, A, i);
+    if (W0 == 4) return dec4<FM>(x[0], x[1], x[2], x[3], T, 8, plain, np);
     if (W0 == 2) return dec2<FM>(x[0], x[1], T, 16, plain, np);
     // W0 == 1: a single leaf
     return ((T.leaf & 1u) || !(x[0] < 0.0f)) ? 0u : 1u;

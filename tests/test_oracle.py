@@ -68,11 +68,34 @@ def test_f_identities():
     assert np.all(O.fmag32(np.zeros(3, np.float32), np.float32([0, 2, 50])) == 0)
 
 
+def _chain(m, k):
+    t = m
+    for _ in range(k):
+        t = 0.427 * t * t if t < 1.0 else max(0.427, t - 0.6932)
+    return t
+
+
 def test_rate1_guard_bound_is_a_lower_bound():
     # the CUDA rate-1 shortcut chains b(t) <= |boxplus(t, t)|; check it here
     t = np.geomspace(1e-20, 1e4, 20000)
     b = np.where(t < 1.0, 0.427 * t * t, np.maximum(0.427, t - 0.6932))
     assert np.all(b <= O.fmag64(t, t) * (1 + 1e-12))
+
+
+def test_rate1_tau_table_matches_its_derivation():
+    """RATE1_TAU[k] (polarsc.cu) must make the k-fold bound chain reach 1e-30."""
+    import os
+    import re
+    src = open(os.path.join(os.path.dirname(__file__), "..", "paper_1204_5882_b200", "csrc",
+                            "polarsc.cu")).read()
+    body = src[src.index("RATE1_TAU[26] = {"):]
+    body = body[:body.index("}")]
+    taus = [float(v) for v in re.findall(r"([0-9.e+-]+)f", body)]
+    assert len(taus) == 26
+    for k, tau in enumerate(taus):
+        assert _chain(np.float32(tau).item(), k) >= 1e-30
+        # and the threshold is not absurdly loose: 1% below it the chain fails
+        assert _chain(tau * 0.99, k) < 1e-30 or tau < 1e-20
 
 
 # ---- SC decoders: naive brute force vs C walk vs numpy recursion

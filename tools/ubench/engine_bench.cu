@@ -79,6 +79,7 @@ __global__ void k_engine(const float *in, const uint8_t *ty_g, float *out, int i
 
 // one warp decodes the four W=256 sub-trees of the c1 code (S = N = 1024)
 // through the product's warp_walk, from shared-memory stage buffers
+template <int FM>
 __global__ void k_c1_warp(const uint8_t *types_g, const float *llr, long long *cyc, uint32_t *out, int reps)
 {
     __shared__ uint8_t ty[2048];
@@ -94,7 +95,7 @@ __global__ void k_c1_warp(const uint8_t *types_g, const float *llr, long long *c
             // stage buffer for width 256 lives at st_end - 512
             for (int q = 0; q < 8; q++) st[2048 - 512 + 32 * q + lane] = llr[256 * sI + 32 * q + lane] + 0.001f * (float)rep;
             __syncwarp();
-            warp_walk<PQ_F_EXACT>(st + 2048, xs, ty, nullptr, 1024, 1024, 0, 0, 0, 2, (uint32_t)sI);
+            warp_walk<FM>(st + 2048, xs, ty, nullptr, 1024, 1024, 0, 0, 0, 2, (uint32_t)sI);
         }
     long long t1 = clock64();
     out[blockIdx.x * 32 + lane] = xs[lane];
@@ -161,13 +162,16 @@ int main()
             cudaMalloc(&dout, 148 * 128);
             cudaMemcpy(dl, lh, 4096, cudaMemcpyHostToDevice);
             cudaMemcpy(dty, tyh, 2048, cudaMemcpyHostToDevice);
-            for (int r = 0; r < 2; r++) k_c1_warp<<<1, 32>>>(dty, dl, cyc, dout, 10);
+            for (int r = 0; r < 2; r++) k_c1_warp<PQ_F_MINSUM><<<1, 32>>>(dty, dl, cyc, dout, 10);
+            cudaMemcpy(&c, cyc, 8, cudaMemcpyDeviceToHost);
+            printf("c1 warp levels, MIN-SUM f: %lld cycles\n", c);
+            for (int r = 0; r < 2; r++) k_c1_warp<PQ_F_EXACT><<<1, 32>>>(dty, dl, cyc, dout, 10);
             cudaMemcpy(&c, cyc, 8, cudaMemcpyDeviceToHost);
             printf("c1 warp levels (4 x W256 sub-trees): %lld cycles\n", c);
             unsigned long long tt[16], cc[16];
             cudaMemcpyFromSymbol(tt, g_ub_time, sizeof tt);
             cudaMemcpyFromSymbol(cc, g_ub_count, sizeof cc);
-            k_c1_warp<<<148, 32>>>(dty, dl, cyc, dout, 10);  // the launch ncu profiles
+            k_c1_warp<PQ_F_EXACT><<<148, 32>>>(dty, dl, cyc, dout, 10);  // the launch ncu profiles
             cudaDeviceSynchronize();
             printf("dec8: %llu calls %.0f cycles/call; dec32: %llu calls %.0f cycles/call\n", cc[0],
                    (double)tt[0] / (cc[0] ? cc[0] : 1), cc[1], (double)tt[1] / (cc[1] ? cc[1] : 1));

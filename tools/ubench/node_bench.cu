@@ -1,0 +1,72 @@
+// Latency of individual lower-band building blocks (one warp, dependent chain).
+#include "../../paper_1204_5882_b200/csrc/polarsc.cu"
+#ifndef FMX
+#define FMX PQ_F_EXACT
+#endif
+
+template <int MODE>
+__global__ void k_node(const float *in, long long *cyc, uint32_t *out, int iters, uint32_t tb0, uint32_t tb1,
+                       uint32_t leaf, int plain)
+{
+    load_log_table();
+    __syncthreads();
+    TypeBits T;
+    T.tb0 = tb0;
+    T.tb1 = tb1;
+    T.leaf = leaf;
+    NodePos np;
+    np.dump = nullptr;
+    np.N = 32;
+    np.d = 0;
+    np.j = 0;
+    float v = in[threadIdx.x & 31];
+    uint32_t acc = 0;
+    long long t0 = clock64();
+    for (int i = 0; i < iters; i++) {
+        uint32_t r;
+        if (MODE == 8) r = dec8<FMX>(v, T, 1, plain != 0, np);
+        else if (MODE == 32) r = dec32<FMX>(v, T, plain != 0, np);
+        else if (MODE == 16) r = dec16<FMX>(v, T, 1, plain != 0, np);
+        else if (MODE == 4) r = dec4<FMX>(v, T, 1, plain != 0, np);
+        else r = dec2<FMX>(v, __shfl_sync(0xffffffffu, v, 1), T, 1, plain != 0, np);
+        acc += r;
+        v = v + 1e-7f * (float)(r & 1u);  // carry a dependency into the next call
+    }
+    long long t1 = clock64();
+    out[threadIdx.x] = acc;
+    if (threadIdx.x == 0) cyc[0] = (t1 - t0) / iters;
+}
+
+int main()
+{
+    float h[32];
+    for (int i = 0; i < 32; i++) h[i] = (i % 3 == 0 ? -1.f : 1.f) * (2.0f + 0.37f * (i % 7));
+    float *in;
+    long long *cyc, c;
+    uint32_t *out;
+    cudaMalloc(&in, 128);
+    cudaMalloc(&cyc, 8);
+    cudaMalloc(&out, 128);
+    cudaMemcpy(in, h, 128, cudaMemcpyHostToDevice);
+    auto run = [&](const char *name, auto kern, uint32_t tb0, uint32_t tb1, uint32_t leaf, int plain) {
+        for (int r = 0; r < 2; r++) kern<<<1, 32>>>(in, cyc, out, 200, tb0, tb1, leaf, plain);
+        cudaMemcpy(&c, cyc, 8, cudaMemcpyDeviceToHost);
+        printf("%-40s %7lld cycles\n", name, c);
+    };
+    // type codes: MIXED 0, R0 1, R1 2, REP 3 -> tb0 = bit0, tb1 = bit1 per heap index
+    // all internal nodes R1: tb0 = 0, tb1 = all
+    run("dec2 R1 (guard)", k_node<2>, 0u, 0xffffffffu, 0u, 0);
+    run("dec2 REP", k_node<2>, 0xffffffffu, 0xffffffffu, 0u, 0);
+    run("dec2 mixed (I,I generic)", k_node<2>, 0u, 0u, 0u, 1);
+    run("dec4 R1", k_node<4>, 0u, 0xffffffffu, 0u, 0);
+    run("dec4 plain (3 mixed)", k_node<4>, 0u, 0u, 0u, 1);
+    run("dec8 R1", k_node<8>, 0u, 0xffffffffu, 0u, 0);
+    run("dec8 plain (7 mixed)", k_node<8>, 0u, 0u, 0u, 1);
+    run("dec16 plain (15 mixed)", k_node<16>, 0u, 0u, 0u, 1);
+    run("dec32 R1", k_node<32>, 0u, 0xffffffffu, 0u, 0);
+    run("dec32 plain (31 mixed)", k_node<32>, 0u, 0u, 0u, 1);
+    // mixed root whose children are R1 (types: h=1 mixed, h>=2 R1)
+    run("dec8 mixed root, R1 children", k_node<8>, 0u, 0xfffffffcu, 0u, 0);
+    run("dec4 mixed root, REP+R1 children", k_node<4>, 0x4u, 0xcu, 0u, 0);
+    printf("err=%s\n", cudaGetErrorString(cudaGetLastError()));
+}
