@@ -27,7 +27,7 @@ __global__ void k_node(const float *in, long long *cyc, uint32_t *out, int iters
         if (MODE == 8) r = dec8<FMX>(v, T, 1, plain != 0, np);
         else if (MODE == 32) r = dec32<FMX>(v, T, plain != 0, np);
         else if (MODE == 16) r = dec16<FMX>(v, T, 1, plain != 0, np);
-        else if (MODE == 4) r = dec4<FMX>(v, T, 1, plain != 0, np);
+        else if (MODE == 4) r = dec4<FMX>(__shfl_sync(0xffffffffu, v, 0), __shfl_sync(0xffffffffu, v, 1), __shfl_sync(0xffffffffu, v, 2), __shfl_sync(0xffffffffu, v, 3), T, 1, plain != 0, np);
         else r = dec2<FMX>(v, __shfl_sync(0xffffffffu, v, 1), T, 1, plain != 0, np);
         acc += r;
         v = v + 1e-7f * (float)(r & 1u);  // carry a dependency into the next call
@@ -68,5 +68,8 @@ int main()
     // mixed root whose children are R1 (types: h=1 mixed, h>=2 R1)
     run("dec8 mixed root, R1 children", k_node<8>, 0u, 0xfffffffcu, 0u, 0);
     run("dec4 mixed root, REP+R1 children", k_node<4>, 0x4u, 0xcu, 0u, 0);
+    // the launch profiled by ncu: 148 warps, dec8 mixed root with R1 children
+    k_node<8><<<148, 32>>>(in, cyc, out, 2000, 0u, 0xfffffffcu, 0u, 0);
+    cudaDeviceSynchronize();
     printf("err=%s\n", cudaGetErrorString(cudaGetLastError()));
 }
