@@ -221,7 +221,9 @@ def main():
     F = args.frames or cfg.frames_per_gpu
     is_bsc = isinstance(cfg.channel, Bsc)
 
-    x, llr, y_bits = gen_frames(cfg, N, rank * F, F)
+    from paper_1204_5882_b200 import dist as D
+    idx = D.shard(F, rank)  # weak scaling: rank r owns frames [rF, (r+1)F)
+    x, llr, y_bits = gen_frames(cfg, N, idx.start, F)
     x_w = torch.from_numpy(pack_bits(x).view(np.int32).copy()).to(dev)
     u_w = polar_transform_words(x_w, n)  # Alice: u = T(x); the decoder reads u at frozen positions
     llr_d = torch.from_numpy(llr).to(dev)
@@ -322,9 +324,7 @@ def main():
         assert err2 == errors, "e2e path decoded differently from the device path"
 
     # statistics off the hot path (NCCL all-reduce of frame errors)
-    stats = torch.tensor([errors, F], dtype=torch.int64, device=dev)
-    if world > 1:
-        dist.all_reduce(stats)
+    stats = D.reduce_stats(torch.tensor([errors, F], dtype=torch.int64, device=dev))
 
     if rank == 0:
         peaks = {}

@@ -14,6 +14,7 @@ GOLDEN = os.path.join(ROOT, "tests", "golden")
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a CUDA device (B200) and libpolarsc.so")
     config.addinivalue_line("markers", "slow: long-running")
+    config.addinivalue_line("markers", "timeout: per-test time limit")
 
 
 def golden(name):
