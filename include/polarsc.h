@@ -41,6 +41,11 @@ extern "C" {
  * approximation named by the north star (no reference counterpart).        */
 #define PQ_F_EXACT 0
 #define PQ_F_MINSUM 1
+/* FAST: the same exact boxplus evaluated with the SFU's ex2/lg2/rcp
+ * approximations (max relative error ~1e-6 vs f64; ~1.7x cheaper); its parity
+ * is the north star's tolerance rule against the f64 oracle, not bit-exactness
+ * with the fp32 mirror.                                                    */
+#define PQ_F_FAST 2
 
 /* options for pq_decoder_set_option */
 #define PQ_OPT_SSC 1          /* 1 (default): skip rate-0/rate-1/repetition sub-trees
@@ -110,6 +115,10 @@ int pq_polar_transform(const uint32_t *in, uint32_t *out, int n, int frames, voi
  * shared g, shared other, warp sub-trees, type staging, rate-1, total,
  * #warp sub-trees, #block nodes, ...}.  Synchronous.  Diagnostics only. */
 int pq_decoder_read_profile(const pq_decoder *h, unsigned long long *out, int frames);
+
+/* Evaluate the signed f (check-node combine) of mode f_mode elementwise on
+ * device arrays: out[i] = f(a[i], b[i]).  Diagnostics / parity tests.     */
+int pq_debug_fmag(int f_mode, const float *a, const float *b, float *out, int n, void *stream);
 
 /* Bytes of device scratch owned by the handle. */
 size_t pq_decoder_workspace_bytes(const pq_decoder *h);

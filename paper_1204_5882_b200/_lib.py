@@ -14,6 +14,7 @@ LIB_PATH = os.path.join(HERE, "libpolarsc.so")
 
 PQ_F_EXACT = 0
 PQ_F_MINSUM = 1
+PQ_F_FAST = 2
 PQ_OPT_SSC = 1
 PQ_OPT_SUBTREE_LOG2 = 2
 PQ_OPT_FMODE = 3
@@ -29,6 +30,7 @@ EXPORTS = (
     "pq_decoder_get_option", "pq_sc_decode_f32", "pq_sc_decode_f32_dump", "pq_sc_decode_bsc",
     "pq_polar_transform", "pq_decoder_workspace_bytes", "pq_decoder_last_launches",
     "pq_decoder_destroy", "pq_last_error", "pq_abi_version", "pq_decoder_read_profile",
+    "pq_debug_fmag",
 )
 
 _lib = None
@@ -62,6 +64,7 @@ def load():
     L.pq_decoder_last_launches.argtypes = [vp]
     L.pq_decoder_destroy.argtypes = [vp]
     L.pq_decoder_read_profile.argtypes = [vp, vp, i]
+    L.pq_debug_fmag.argtypes = [i, vp, vp, vp, i, vp]
     L.pq_last_error.restype = ctypes.c_char_p
     L.pq_abi_version.restype = ctypes.c_int
     for name in EXPORTS:

@@ -98,7 +98,8 @@ def _check_words(t, frames, wpf, name):
         raise ValueError(f"{name} holds {t.numel()} words, need {frames * wpf}")
 
 
-F_MODES = {"exact": _lib.PQ_F_EXACT, "min-sum": _lib.PQ_F_MINSUM, "minsum": _lib.PQ_F_MINSUM}
+F_MODES = {"exact": _lib.PQ_F_EXACT, "fast": _lib.PQ_F_FAST, "min-sum": _lib.PQ_F_MINSUM,
+           "minsum": _lib.PQ_F_MINSUM}
 
 
 class ScDecoder:
@@ -110,7 +111,7 @@ class ScDecoder:
                  ssc: bool = True, subtree_log2: int = 0, device=None):
         self.device = _require_cuda(device)
         if f_mode not in F_MODES:
-            raise ValueError(f"unknown f mode {f_mode!r} (exact | min-sum)")
+            raise ValueError(f"unknown f mode {f_mode!r} (exact | fast | min-sum)")
         L = _lib.load()
         self.code = code
         self.n = code.n
@@ -213,6 +214,19 @@ class ScDecoder:
             self.close()
         except Exception:
             pass
+
+
+def f_device(a, b, f_mode: str = "exact"):
+    """The decoder's signed f on device arrays (diagnostics / parity tests)."""
+    _require_cuda()
+    if not (a.is_cuda and b.is_cuda and a.dtype == torch.float32 and b.dtype == torch.float32):
+        raise ValueError("a, b must be float32 CUDA tensors")
+    a, b = a.contiguous(), b.contiguous()
+    out = torch.empty_like(a)
+    rc = _lib.load().pq_debug_fmag(F_MODES[f_mode], _ptr(a), _ptr(b), _ptr(out), a.numel(),
+                                   _stream_ptr(None))
+    _lib.check(rc, "pq_debug_fmag")
+    return out
 
 
 # --------------------------------------------------------------------------

@@ -306,3 +306,64 @@ def test_ssc_equals_plain_on_large_random(cuda):
     a, _ = gpu_decode(cuda, code, llr, fz, ssc=True)
     b, _ = gpu_decode(cuda, code, llr, fz, ssc=False)
     assert np.array_equal(a, b)
+
+
+# --------------------------------------------------------------------------
+# the f function itself, and the FAST (SFU) mode
+
+def test_f_exact_is_the_mirror_and_fast_is_accurate(cuda):
+    import torch
+    from paper_1204_5882_b200.polar_core import f_device
+    rng = np.random.default_rng(11)
+    for lo, hi in [(1e-7, 1e-3), (1e-3, 1.0), (1.0, 8.0), (8.0, 40.0), (40.0, 1e3), (1e3, 1e8), (1e-7, 1e8)]:
+        a = np.exp(rng.uniform(np.log(lo), np.log(hi), 200000)).astype(np.float32)
+        b = np.exp(rng.uniform(np.log(lo), np.log(hi), 200000)).astype(np.float32)
+        a *= np.where(rng.random(a.size) < 0.5, -1, 1).astype(np.float32)
+        ta, tb = torch.from_numpy(a).to(cuda), torch.from_numpy(b).to(cuda)
+        ex = f_device(ta, tb, "exact").cpu().numpy()
+        mirror = O.fmag32(np.abs(a), np.abs(b)) * np.sign(a) * np.sign(b)
+        assert np.array_equal(ex, mirror.astype(np.float32))
+        ref = O.fmag64(np.abs(a).astype(np.float64), np.abs(b).astype(np.float64))
+        fa = f_device(ta, tb, "fast").cpu().numpy().astype(np.float64)
+        assert np.all(np.sign(fa) == np.sign(a) * np.sign(b))
+        assert np.max(np.abs(np.abs(fa) - ref) / ref) < 2e-6, (lo, hi)
+
+
+@pytest.mark.parametrize("key", ["c1", "c2", "c3", "c4"])
+def test_config_parity_fast_f(cuda, key):
+    """FAST f: bit-exact decisions vs the f64 oracle on every frame without a
+    near-tie decision LLR; FER within the binomial interval."""
+    if key not in K.available_configs():
+        pytest.skip(f"{key}.pqct not built")
+    cfg, code, x, u_true, llr = config_batch(key, CFG_FRAMES[key])
+    ref64, mi64 = oracle_batch(code, llr, u_true, 64)
+    u, xh = gpu_decode(cuda, code, llr, u_true, fmode="fast")
+    clean = mi64 >= 1e-4
+    assert np.array_equal(u[clean], ref64[clean])
+    ok_gpu = np.all(u == u_true, axis=1)
+    ok64 = np.all(ref64 == u_true, axis=1)
+    F = len(ok_gpu)
+    fer, fer64 = 1 - ok_gpu.mean(), 1 - ok64.mean()
+    assert abs(fer - fer64) <= 3 * np.sqrt(max(fer64 * (1 - fer64), 1.0 / F) / F)
+
+
+@pytest.mark.parametrize("n", [6, 10, 13])
+def test_stage_llrs_fast_within_tolerance(cuda, n):
+    """FAST f stage LLRs within 1e-4 relative (+1e-6) of the f64 oracle."""
+    rng = np.random.default_rng(n + 100)
+    code = random_code(n, 0.45, rng)
+    F, N = 4, 1 << n
+    llr = rng.normal(0.8, 1.8, (F, N)).astype(np.float32)
+    fz = rng.integers(0, 2, (F, N)).astype(np.uint8)
+    dec = ScDecoder(code, max_frames=F, f_mode="fast")
+    u, _, dump = dec.decode_dump(to_dev(llr, cuda), words_dev(fz, cuda))
+    dump = dump.cpu().numpy()
+    u = from_words(u, N)
+    for f in range(F):
+        sign = 1.0 - 2.0 * node_flips(code.frozen_mask, fz[f], n)
+        u64, _, st64, lf64 = O.sc_decode(code.frozen_mask, llr[f].astype(np.float64), fz[f], 64,
+                                         dump=True, leaf=True)
+        if np.min(np.abs(lf64[code.frozen_mask == 0]), initial=np.inf) >= 1e-4:
+            assert np.array_equal(u[f], u64)
+            got = dump[f].astype(np.float64) * sign
+            assert np.all(np.abs(got - st64) <= 1e-4 * np.abs(st64) + 1e-6)
