@@ -1003,9 +1003,26 @@ __global__ void __launch_bounds__(256, 2) sc_decode_kernel(DecParams p)
                 PROF_MARK(PR_TYPES);
                 // entering a shared-memory sub-tree: stage its node types
                 __syncthreads();
-                for (uint32_t q = 1 + tid; q < 2 * S; q += nthr) {
-                    const int e = 31 - __clz(q);
-                    sm.ty[q] = __ldg(p.types + ((size_t)1 << (dS + e)) + ((size_t)j << e) + (q - (1u << e)));
+                if (S >= 128) {
+                    // levels e >= 4 are 16-byte aligned runs in both layouts: copy
+                    // them as uint4 (4 loads per thread at S = 8192 instead of 64)
+                    if (tid < 15) {
+                        const uint32_t q = 1 + tid;
+                        const int e = 31 - __clz(q);
+                        sm.ty[q] = __ldg(p.types + ((size_t)1 << (dS + e)) + ((size_t)j << e) + (q - (1u << e)));
+                    }
+                    for (uint32_t c = tid; c < (2 * S - 16) / 16; c += nthr) {
+                        const uint32_t q = 16 + 16 * c;
+                        const int e = 31 - __clz(q);
+                        const uint4 *src = reinterpret_cast<const uint4 *>(
+                            p.types + ((size_t)1 << (dS + e)) + ((size_t)j << e) + (q - (1u << e)));
+                        *reinterpret_cast<uint4 *>(sm.ty + q) = __ldg(src);
+                    }
+                } else {
+                    for (uint32_t q = 1 + tid; q < 2 * S; q += nthr) {
+                        const int e = 31 - __clz(q);
+                        sm.ty[q] = __ldg(p.types + ((size_t)1 << (dS + e)) + ((size_t)j << e) + (q - (1u << e)));
+                    }
                 }
             }
             if (W <= WMAX) {
