@@ -1024,6 +1024,7 @@ __global__ void __launch_bounds__(256, 2) sc_decode_kernel(DecParams p)
                         sm.ty[q] = __ldg(p.types + ((size_t)1 << (dS + e)) + ((size_t)j << e) + (q - (1u << e)));
                     }
                 }
+                __syncthreads();  // the types are read right below (before the next step's barrier)
             }
             if (W <= WMAX) {
                 PROF_MARK(PR_WARP);
