@@ -277,12 +277,7 @@ __device__ __forceinline__ bool rate1_guard(float m, int k) { return m >= RATE1_
 // ---------------------------------------------------------------------------
 // node types (host computes them from the frozen mask; heap order)
 
-// SPC: single parity check -- only the first leaf frozen (W >= 4).  Its SC
-// decode is a chain: the left child is SPC(W/2) (REP at W = 2), the right child
-// rate-1; decoded by spc_lanes() below with no per-node type dispatch.  Code
-// that does not special-case SPC treats it as MIXED (its children's types
-// then drive the generic recursion), which is equally exact.
-enum : uint8_t { NT_MIXED = 0, NT_RATE0 = 1, NT_RATE1 = 2, NT_REP = 3, NT_SPC = 4 };
+enum : uint8_t { NT_MIXED = 0, NT_RATE0 = 1, NT_RATE1 = 2, NT_REP = 3 };
 
 struct DecParams {
     int n, log2S, plain, frames;
@@ -408,11 +403,11 @@ __device__ unsigned long long g_ub_time[16], g_ub_count[16];
 // frozen flag in `leaf` (bit h - 32).  Sub-trees narrower than 32 (blocks
 // shorter than 32 only) sit at the leftmost node of that width.
 struct TypeBits {
-    uint32_t tb0, tb1, tb2, leaf;
+    uint32_t tb0, tb1, leaf;
 };
 __device__ __forceinline__ uint32_t tget(const TypeBits &T, int h)
 {
-    return ((T.tb0 >> h) & 1u) | (((T.tb1 >> h) & 1u) << 1) | (((T.tb2 >> h) & 1u) << 2);
+    return ((T.tb0 >> h) & 1u) | (((T.tb1 >> h) & 1u) << 1);
 }
 
 // absolute position of a node, for the plain-mode stage dump
@@ -538,66 +533,6 @@ __device__ __forceinline__ bool lanes_special(float v, int W, uint32_t t, uint32
     return false;
 }
 
-template <int FM>
-__device__ __forceinline__ uint32_t dec16(float v, const TypeBits &T, int h, bool plain, const NodePos &np);
-template <int FM>
-__device__ __noinline__ uint32_t dec8(float v, const TypeBits T, int h, bool plain, const NodePos np);
-
-// SPC node of width W in {8, 16, 32} at heap index h, lane i holds element i.
-// SC on an SPC node is a chain: f-steps down the left spine (SPC(W/2), ...,
-// REP at width 2), then on the way up each right child is rate-1: its bits
-// are the hard decisions of the g-values when the rate-1 guard holds
-// (otherwise the generic decoder takes that child).  The (a, b) operand pairs
-// of every level stay in registers; no per-node type dispatch.
-template <int FM>
-__device__ __noinline__ uint32_t spc_lanes(float v, int W, const TypeBits T, int h, const NodePos np)
-{
-    const unsigned FULL = 0xffffffffu;
-    const int lane = threadIdx.x & 31;
-    float a[4], b[4];
-    int hk = h;  // heap index of the current spine node
-    // descend: level k has width 32 >> k
-#pragma unroll
-    for (int k = 0; k < 4; k++) {
-        const int w = 32 >> k;
-        if (w <= W) {
-            a[k] = v;
-            b[k] = __shfl_down_sync(FULL, v, w / 2);
-            v = pq_f<FM>(a[k], b[k]);
-            hk = 2 * hk;
-        }
-    }
-    // bottom: width-2 repetition node (frozen, info) on lanes 0, 1
-    const float v0 = __shfl_sync(FULL, v, 0), v1 = __shfl_sync(FULL, v, 1);
-    uint32_t x = (v1 + v0) < 0.0f ? 3u : 0u;
-    // ascend: g into the rate-1 right child, combine
-#pragma unroll
-    for (int k = 3; k >= 0; k--) {
-        const int w = 32 >> k, hw = w / 2;
-        if (w <= W) {
-            hk >>= 1;  // back at the level-k spine node; its right child is 2hk+1
-            const float r = pq_g(a[k], b[k], (x >> (lane & (hw - 1))) & 1u);
-            const bool ok = __all_sync(FULL, lane >= hw || fabsf(r) >= RATE1_TAU[ilog2((uint32_t)hw)]);
-            uint32_t xr = __ballot_sync(FULL, lane < hw && r < 0.0f) & lowmask(hw);
-            if (!ok) {
-                const NodePos z = {nullptr, 0, 0, 0};
-                if (hw == 16) {
-                    xr = dec16<FM>(r, T, 2 * hk + 1, false, z);
-                } else if (hw == 8) {
-                    xr = dec8<FM>(r, T, 2 * hk + 1, false, z);
-                } else if (hw == 4) {
-                    xr = dec4<FM>(__shfl_sync(FULL, r, 0), __shfl_sync(FULL, r, 1), __shfl_sync(FULL, r, 2),
-                                  __shfl_sync(FULL, r, 3), T, 2 * hk + 1, false, z);
-                } else {
-                    xr = dec2<FM>(__shfl_sync(FULL, r, 0), __shfl_sync(FULL, r, 1), T, 2 * hk + 1, false, z);
-                }
-            }
-            x = (x ^ xr) | (xr << hw);
-        }
-    }
-    return x;
-}
-
 // W = 8 node, lane i holds element i (lanes 0..7).  One copy (noinline):
 // lane-parallel f/g step, then the width-4 children in registers.
 template <int FM>
@@ -606,10 +541,6 @@ __device__ __noinline__ uint32_t dec8(float v, const TypeBits T, int h, bool pla
     UB_BEGIN();
     const unsigned FULL = 0xffffffffu;
     uint32_t bits;
-    if (!plain && tget(T, h) == NT_SPC) {
-        UB_END(0);
-        return spc_lanes<FM>(v, 8, T, h, np);
-    }
     if (!plain && lanes_special(v, 8, tget(T, h), bits)) {
         UB_END(0);
         return bits;
@@ -637,7 +568,6 @@ __device__ __forceinline__ uint32_t dec16(float v, const TypeBits &T, int h, boo
 {
     const int lane = threadIdx.x & 31;
     uint32_t bits;
-    if (!plain && tget(T, h) == NT_SPC) return spc_lanes<FM>(v, 16, T, h, np);
     if (!plain && lanes_special(v, 16, tget(T, h), bits)) return bits;
     const float b = __shfl_down_sync(0xffffffffu, v, 8);
     uint32_t xl = 0, xr = 0;
@@ -669,7 +599,6 @@ __device__ __forceinline__ uint32_t dec32_body(float v, const TypeBits T, bool p
 {
     const int lane = threadIdx.x & 31;
     uint32_t bits;
-    if (!plain && tget(T, 1) == NT_SPC) return spc_lanes<FM>(v, 32, T, 1, np);
     if (!plain && lanes_special(v, 32, tget(T, 1), bits)) return bits;
     const float b = __shfl_down_sync(0xffffffffu, v, 16);
     uint32_t xl = 0, xr = 0;
@@ -702,7 +631,6 @@ __device__ __forceinline__ TypeBits load_typebits(const uint8_t *ty, uint32_t ro
     TypeBits T;
     T.tb0 = __ballot_sync(FULL, tint & 1u);
     T.tb1 = __ballot_sync(FULL, tint & 2u);
-    T.tb2 = __ballot_sync(FULL, tint & 4u);
     T.leaf = __ballot_sync(FULL, tl == NT_RATE0);
     return T;
 }
@@ -1559,13 +1487,11 @@ int pq_decoder_set_frozen_mask(pq_decoder *h, const uint8_t *mask)
     std::vector<uint8_t> ty(2 * (size_t)N, NT_MIXED);
     std::vector<uint32_t> nfrozen(2 * (size_t)N);
     std::vector<uint8_t> lastinfo(2 * (size_t)N);
-    std::vector<uint8_t> firstfrozen(2 * (size_t)N);
     for (uint32_t i = 0; i < N; i++) {
         if (mask[i] > 1) return set_err(-1, "frozen mask entries must be 0 or 1 (index %u)", i);
         const size_t q = N + i;
         nfrozen[q] = mask[i];
         lastinfo[q] = mask[i] ? 0 : 1;
-        firstfrozen[q] = mask[i] ? 1 : 0;
         ty[q] = mask[i] ? NT_RATE0 : NT_RATE1;
     }
     for (size_t q = N - 1; q >= 1; q--) {
@@ -1573,11 +1499,9 @@ int pq_decoder_set_frozen_mask(pq_decoder *h, const uint8_t *mask)
         const uint32_t W = (uint32_t)(N >> (31 - __builtin_clz((uint32_t)q)));
         nfrozen[q] = nfrozen[l] + nfrozen[r];
         lastinfo[q] = lastinfo[r];
-        firstfrozen[q] = firstfrozen[l];
         if (nfrozen[q] == W) ty[q] = NT_RATE0;
         else if (nfrozen[q] == 0) ty[q] = NT_RATE1;
         else if (nfrozen[q] == W - 1 && lastinfo[q]) ty[q] = NT_REP;
-        else if (nfrozen[q] == 1 && firstfrozen[q] && W >= 4) ty[q] = NT_SPC;
         else ty[q] = NT_MIXED;
     }
     ty[0] = NT_MIXED;
