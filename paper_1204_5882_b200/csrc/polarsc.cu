@@ -40,7 +40,6 @@
 #include <stdlib.h>
 #include <string.h>
 
-#include <algorithm>
 #include <string>
 #include <vector>
 
@@ -292,11 +291,6 @@ struct DecParams {
     uint32_t *X;                 // [F][wpf] out: shifted x-hat partial sums
     float *dump;                 // [F][n+1][N] stage dump (plain mode), or null
     unsigned long long *prof;    // [F][PQ_PROF_SLOTS] clock64 cycles per step class, or null
-    const uint8_t *prog;         // width-32 sub-tree programs (SSC), concatenated in node order
-    const uint32_t *prog_off;    // [N/32 + 1] program start offsets
-    const uint8_t *plain_prog;   // the universal plain-SC program of a width-32 node
-    const uint32_t *fmask;       // [wpf] packed frozen mask (leaf flags for the programs)
-    uint32_t prog_cap;           // shared-memory bytes reserved for one S-sub-tree's programs
 };
 
 // step classes for the optional per-frame cycle profile (PQ_OPT_PROFILE)
@@ -348,8 +342,6 @@ struct Smem {
     float *st;
     uint32_t *xs;
     uint8_t *ty;
-    uint32_t *poff;  // [S/32 + 1] program offsets of the current S-sub-tree (relative)
-    uint8_t *prog;   // its programs (prog_cap bytes)
 };
 
 // stage pointer for a node of width W at depth d >= 1
@@ -526,14 +518,15 @@ __device__ __forceinline__ bool lanes_special(float v, int W, uint32_t t, uint32
         }
     }
     if (t == NT_REP) {
-        // SC's g-chain with zero partial sums, in its pairing order:
-        // r_i = L[i + w/2] + L[i], halving (shuffle tree, values stay in lanes)
-        float sum = v;
-        for (int hh = W / 2; hh >= 1; hh >>= 1) {
-            const float other = __shfl_down_sync(FULL, sum, hh);
-            sum = other + sum;
-        }
-        float x[1] = {__shfl_sync(FULL, sum, 0)};
+        // all values to every lane, then SC's g-chain sum in its pairing order
+        float x[32];
+#pragma unroll
+        for (int i = 0; i < 32; i++) x[i] = i < W ? __shfl_sync(FULL, v, i) : 0.0f;
+#pragma unroll
+        for (int hh = 16; hh >= 1; hh >>= 1)
+            if (hh < W)
+#pragma unroll
+                for (int i = 0; i < hh; i++) x[i] = x[i + hh] + x[i];
         bits = x[0] < 0.0f ? lowmask(W) : 0u;
         return true;
     }
@@ -571,7 +564,7 @@ __device__ __noinline__ uint32_t dec8(float v, const TypeBits T, int h, bool pla
 }
 
 template <int FM>
-__device__ __noinline__ uint32_t dec16(float v, const TypeBits T, int h, bool plain, const NodePos np)
+__device__ __forceinline__ uint32_t dec16(float v, const TypeBits &T, int h, bool plain, const NodePos &np)
 {
     const int lane = threadIdx.x & 31;
     uint32_t bits;
@@ -739,144 +732,6 @@ __device__ __forceinline__ float block_min(float v, float *red)
 // ---------------------------------------------------------------------------
 // the per-frame tree walk
 
-// ---------------------------------------------------------------------------
-// Width-32 sub-trees as precompiled programs.  The node types of a code are
-// static, so the host compiles every width-32 sub-tree into a short op list
-// (post-order: F/FZ, left child, SL, G, right child, C; R0 / R1 / REP / D2
-// leaves of the list).  run32() executes it with all control resolved ahead of
-// time: node values live in registers (A: root, lane i = element i; B: the
-// current node of every depth e >= 1 at lanes o(e) .. o(e) + 32>>e), the f
-// operand pairs in Ca/Cb at the child's lanes, left-child partial sums of
-// every depth packed in one uniform word XL at bit offset o(e).
-
-enum : uint32_t { OP_END = 0, OP_F = 1, OP_FZ = 2, OP_SL = 3, OP_G = 4, OP_C = 5, OP_R0 = 6, OP_R1 = 7,
-                  OP_REP = 8, OP_D2 = 9 };
-
-template <int FM>
-__device__ __noinline__ uint32_t r1_fallback(float v, int w, const uint8_t *ty, uint32_t lh, int h, int plain_i)
-{
-    // rate-1 node whose guard failed: generic (exact) decode of that node;
-    // v already holds its values at lanes 0 .. w-1
-    const TypeBits T = load_typebits(ty, lh, 32, plain_i != 0);
-    const NodePos z = {nullptr, 0, 0, 0};
-    const unsigned FULL = 0xffffffffu;
-    if (w == 32) return dec32<FM>(v, T, false, z);
-    if (w == 16) return dec16<FM>(v, T, h, false, z);
-    if (w == 8) return dec8<FM>(v, T, h, false, z);
-    if (w == 4)
-        return dec4<FM>(__shfl_sync(FULL, v, 0), __shfl_sync(FULL, v, 1), __shfl_sync(FULL, v, 2),
-                        __shfl_sync(FULL, v, 3), T, h, false, z);
-    return dec2<FM>(__shfl_sync(FULL, v, 0), __shfl_sync(FULL, v, 1), T, h, false, z);
-}
-
-template <int FM>
-__device__ __noinline__ uint32_t run32(float A, const uint8_t *prog, uint32_t leaf, const uint8_t *ty, uint32_t lh,
-                                       float *dump, uint32_t N, int d_root, uint32_t j_root, int plain_i)
-{
-    const unsigned FULL = 0xffffffffu;
-    const int lane = threadIdx.x & 31;
-    float B = 0.0f, Ca = 0.0f, Cb = 0.0f;
-    uint32_t XL = 0, xnode = 0, j = 0;
-    for (int pc = 0;; pc++) {
-        const uint32_t op = prog[pc];
-        const uint32_t code = op & 15u;
-        const int e = (int)(op >> 4);
-        if (code == OP_END) return xnode;
-        switch (code) {
-        case OP_F:
-        case OP_FZ: {
-            const int hw = 16 >> e, o = eng_off(e), oc = eng_off(e + 1);
-            const float P = e == 0 ? A : B;
-            const int src = o + (lane - oc);
-            const float a = __shfl_sync(FULL, P, src & 31), b = __shfl_sync(FULL, P, (src + hw) & 31);
-            const bool inc = lane >= oc && lane < oc + hw;
-            Ca = inc ? a : Ca;
-            Cb = inc ? b : Cb;
-            j = 2 * j;
-            if (code == OP_F) {
-                const float fv = pq_f<FM>(a, b);
-                B = inc ? fv : B;
-                if (dump && inc)
-                    dump[(size_t)(d_root + e + 1) * N + ((size_t)(j_root << (e + 1)) + j) * hw + (lane - oc)] = fv;
-            } else {
-                xnode = 0;
-            }
-            break;
-        }
-        case OP_SL: {
-            const int o = eng_off(e);
-            XL = (XL & ~(lowmask(32 >> e) << o)) | (xnode << o);
-            break;
-        }
-        case OP_G: {
-            const int hw = 16 >> e, oc = eng_off(e + 1);
-            const bool inc = lane >= oc && lane < oc + hw;
-            const float gv = pq_g(Ca, Cb, (XL >> lane) & 1u);
-            B = inc ? gv : B;
-            j = j + 1;
-            if (dump && inc)
-                dump[(size_t)(d_root + e + 1) * N + ((size_t)(j_root << (e + 1)) + j) * hw + (lane - oc)] = gv;
-            break;
-        }
-        case OP_C: {
-            const int hw = 16 >> e;
-            const uint32_t xl = (XL >> eng_off(e + 1)) & lowmask(hw);
-            xnode = (xl ^ xnode) | (xnode << hw);
-            j >>= 1;
-            break;
-        }
-        case OP_R0: xnode = 0; break;
-        case OP_R1: {
-            const int w = 32 >> e, o = eng_off(e);
-            const float P = e == 0 ? A : B;
-            const bool in = lane >= o && lane < o + w;
-            const bool ok = __all_sync(FULL, !in || fabsf(P) >= RATE1_TAU[5 - e]);
-            const uint32_t neg = __ballot_sync(FULL, in && P < 0.0f);
-            if (ok) {
-                xnode = (neg >> o) & lowmask(w);
-            } else {
-                const float v = __shfl_sync(FULL, P, (lane + o) & 31);
-                xnode = r1_fallback<FM>(v, w, ty, lh, (1 << e) + (int)j, plain_i);
-            }
-            break;
-        }
-        case OP_REP: {
-            const int w = 32 >> e, o = eng_off(e);
-            float sum = e == 0 ? A : B;
-            for (int hh = w / 2; hh >= 1; hh >>= 1) {
-                const float other = __shfl_down_sync(FULL, sum, hh);
-                sum = other + sum;
-            }
-            xnode = __shfl_sync(FULL, sum, o) < 0.0f ? lowmask(w) : 0u;
-            break;
-        }
-        default: {  // OP_D2: width-2 node at depth 4 (lanes 28, 29); type in the high bits
-            const uint32_t t = (uint32_t)e & 3u;
-            const float L0 = __shfl_sync(FULL, B, 28), L1 = __shfl_sync(FULL, B, 29);
-            if (t == NT_RATE0) {
-                xnode = 0;
-            } else if (t == NT_REP) {
-                xnode = (L1 + L0) < 0.0f ? 3u : 0u;
-            } else if (t == NT_RATE1 && fminf(fabsf(L0), fabsf(L1)) >= 1.5303335787713972e-15f) {
-                xnode = (L0 < 0.0f ? 1u : 0u) | (L1 < 0.0f ? 2u : 0u);
-            } else {
-                const bool fa = (leaf >> (2 * j)) & 1u, fb = (leaf >> (2 * j + 1)) & 1u;
-                const float l = pq_f<FM>(L0, L1);
-                const uint32_t u0 = fa ? 0u : (l < 0.0f ? 1u : 0u);
-                const float r = pq_g(L0, L1, u0);
-                const uint32_t u1 = fb ? 0u : (r < 0.0f ? 1u : 0u);
-                if (dump && lane == 0) {
-                    dump[(size_t)(d_root + 5) * N + (j_root << 5) + 2 * j] = l;
-                    dump[(size_t)(d_root + 5) * N + (j_root << 5) + 2 * j + 1] = r;
-                }
-                xnode = (u0 ^ u1) | (u1 << 1);
-            }
-            break;
-        }
-        }
-    }
-}
-
 // One warp decodes the sub-tree rooted at (d0, j0), width 32 <= W0 <= 256,
 // inside the shared-memory sub-tree: node values in the shared stage buffers
 // (width W at st_end - 2W), partial sums in xs (bit position (jW) mod S).
@@ -886,8 +741,7 @@ __device__ __noinline__ uint32_t run32(float A, const uint8_t *prog, uint32_t le
 // mirrors the block walk, with __syncwarp instead of __syncthreads.
 template <int FM>
 __device__ __noinline__ void warp_walk(float *st_end, uint32_t *xs, const uint8_t *ty, float *dump, uint32_t N,
-                                       uint32_t S, int dS, uint32_t jS, int plain_i, int d0, uint32_t j0,
-                                       const uint8_t *prog, const uint32_t *poff, const uint32_t *mask_g)
+                                       uint32_t S, int dS, uint32_t jS, int plain_i, int d0, uint32_t j0)
 {
     const unsigned FULL = 0xffffffffu;
     const int lane = threadIdx.x & 31;
@@ -911,10 +765,13 @@ __device__ __noinline__ void warp_walk(float *st_end, uint32_t *xs, const uint8_
             }
             if (W == 32) {
                 const float v = nd[lane];
-                // this width-32 node's program (plain mode: the one universal program)
-                const uint32_t qloc = j & ((S >> 5) - 1);
-                const uint8_t *pg = plain ? prog : prog + poff[qloc];
-                const uint32_t bits = run32<FM>(v, pg, __ldg(mask_g + j), ty, lh, dump, N, d, j, plain_i);
+                const TypeBits T = load_typebits(ty, lh, 32, plain);
+                NodePos np;
+                np.dump = dump;
+                np.N = N;
+                np.d = d;
+                np.j = j;
+                const uint32_t bits = dec32<FM>(v, T, plain, np);
                 if (lane == 0) xs[pos >> 5] = bits;
                 __syncwarp();
                 entering = false;
@@ -1050,12 +907,8 @@ __global__ void __launch_bounds__(256, 2) sc_decode_kernel(DecParams p)
     sm.xs = (uint32_t *)(sm.st + 2 * S);
     const uint32_t SW = S >= 32 ? S / 32 : 1;
     sm.ty = (uint8_t *)(sm.xs + SW);
-    sm.poff = (uint32_t *)(sm.ty + 2 * S);
-    sm.prog = (uint8_t *)(sm.poff + (S >= 32 ? S / 32 : 1) + 1);
 
     load_log_table();
-    if (p.plain && S >= 32)
-        for (uint32_t b = threadIdx.x; b < 128; b += blockDim.x) sm.prog[b] = __ldg(p.plain_prog + b);
     __syncthreads();
     const uint32_t frame = blockIdx.x;
     FrameCtx fc;
@@ -1171,14 +1024,6 @@ __global__ void __launch_bounds__(256, 2) sc_decode_kernel(DecParams p)
                         sm.ty[q] = __ldg(p.types + ((size_t)1 << (dS + e)) + ((size_t)j << e) + (q - (1u << e)));
                     }
                 }
-                if (!p.plain && S >= 32) {
-                    // this S-sub-tree's width-32 programs, contiguous in the global list
-                    const uint32_t q0 = j * (S >> 5), nq = S >> 5;
-                    const uint32_t g0 = __ldg(p.prog_off + q0);
-                    for (uint32_t k = tid; k <= nq; k += nthr) sm.poff[k] = __ldg(p.prog_off + q0 + k) - g0;
-                    const uint32_t len = __ldg(p.prog_off + q0 + nq) - g0;
-                    for (uint32_t b = tid; b < len; b += nthr) sm.prog[b] = __ldg(p.prog + g0 + b);
-                }
                 __syncthreads();  // the types are read right below (before the next step's barrier)
             }
             if (W <= WMAX) {
@@ -1196,8 +1041,7 @@ __global__ void __launch_bounds__(256, 2) sc_decode_kernel(DecParams p)
                             for (uint32_t i = tid & 31; i < W; i += 32) dst[i] = chan_load(p, fc, i);
                             __syncwarp();
                         }
-                        warp_walk<FM>(sm.st + 2 * S, sm.xs, sm.ty, fc.dump, N, S, dS, wc.jS, p.plain, d, j, sm.prog,
-                                      sm.poff, p.fmask);
+                        warp_walk<FM>(sm.st + 2 * S, sm.xs, sm.ty, fc.dump, N, S, dS, wc.jS, p.plain, d, j);
                     } else {
                         const float *src = chan ? nullptr : stage_ptr(p, fc, sm, W);
                         warp_small<FM>(src, chan, p, fc, lh, wc, sm.xs, pos, (int)W);
@@ -1493,52 +1337,7 @@ struct pq_decoder {
     int last_launches;
     int profile;
     unsigned long long *d_prof;
-    uint8_t *d_prog;
-    uint32_t *d_prog_off;
-    uint8_t *d_plain_prog;
-    uint32_t prog_max[16];  // max program bytes of one S-sub-tree, per log2 S
 };
-
-static uint32_t prog_cap_for(const pq_decoder *h, int log2S)
-{
-    uint32_t m = h->prog_max[log2S < 16 ? log2S : 15];
-    if (m < 128) m = 128;  // the universal plain program
-    return (m + 15u) & ~15u;
-}
-
-static size_t dec_smem_bytes(uint32_t S, uint32_t prog_cap)
-{
-    const uint32_t SW = S >= 32 ? S / 32 : 1;
-    return (size_t)8 * S + (size_t)SW * 4 + (size_t)2 * S + (size_t)(SW + 1) * 4 + prog_cap;
-}
-
-// Compile the width-32 sub-tree rooted at heap index hidx (depth e below it)
-// into the op list run32() executes (see the OP_* enum).
-static void gen_prog(const std::vector<uint8_t> &ty, size_t hidx, int e, bool plain, std::vector<uint8_t> &out)
-{
-    const uint32_t W = 32u >> e;
-    const uint8_t t = ty[hidx];
-    if (W == 2) {
-        out.push_back((uint8_t)(OP_D2 | ((plain ? NT_MIXED : (t & 3u)) << 4)));
-        return;
-    }
-    if (!plain) {
-        if (t == NT_RATE0) { out.push_back((uint8_t)(OP_R0 | (e << 4))); return; }
-        if (t == NT_RATE1) { out.push_back((uint8_t)(OP_R1 | (e << 4))); return; }
-        if (t == NT_REP) { out.push_back((uint8_t)(OP_REP | (e << 4))); return; }
-    }
-    const bool l0 = !plain && ty[2 * hidx] == NT_RATE0, r0 = !plain && ty[2 * hidx + 1] == NT_RATE0;
-    out.push_back((uint8_t)((l0 ? OP_FZ : OP_F) | (e << 4)));
-    if (!l0) gen_prog(ty, 2 * hidx, e + 1, plain, out);
-    out.push_back((uint8_t)(OP_SL | ((e + 1) << 4)));
-    if (r0) {
-        out.push_back((uint8_t)(OP_R0 | ((e + 1) << 4)));
-    } else {
-        out.push_back((uint8_t)(OP_G | (e << 4)));
-        gen_prog(ty, 2 * hidx + 1, e + 1, plain, out);
-    }
-    out.push_back((uint8_t)(OP_C | (e << 4)));
-}
 
 static int choose_log2S(const pq_decoder *h, int frames)
 {
@@ -1550,11 +1349,18 @@ static int choose_log2S(const pq_decoder *h, int frames)
     const int per_sm = (frames + h->sm_count - 1) / h->sm_count;
     int best = 6;
     for (int k = 6; k <= 14; k++) {
-        const size_t bytes = dec_smem_bytes(1u << k, prog_cap_for(h, k));
+        const size_t S = (size_t)1 << k;
+        const size_t bytes = 8 * S + (S / 32) * 4 + 2 * S;
         if ((size_t)per_sm * bytes <= 200 * 1024) best = k;
     }
     if (best > h->n) best = h->n;
     return best;
+}
+
+static size_t dec_smem_bytes(uint32_t S)
+{
+    const uint32_t SW = S >= 32 ? S / 32 : 1;
+    return (size_t)8 * S + (size_t)SW * 4 + (size_t)2 * S;
 }
 
 extern "C" {
@@ -1619,9 +1425,6 @@ int pq_decoder_destroy(pq_decoder *h)
     cudaFree(h->d_x);
     cudaFree(h->d_scr);
     cudaFree(h->d_prof);
-    cudaFree(h->d_prog);
-    cudaFree(h->d_prog_off);
-    cudaFree(h->d_plain_prog);
     delete h;
     return 0;
 }
@@ -1705,49 +1508,9 @@ int pq_decoder_set_frozen_mask(pq_decoder *h, const uint8_t *mask)
     std::vector<uint32_t> words(h->wpf, 0);
     for (uint32_t i = 0; i < N; i++)
         if (mask[i]) words[i >> 5] |= 1u << (i & 31);
-    // width-32 sub-tree programs (N >= 32)
-    std::vector<uint8_t> prog;
-    std::vector<uint32_t> poff;
-    std::vector<uint8_t> plain;
-    memset(h->prog_max, 0, sizeof h->prog_max);
-    if (N >= 32) {
-        const int n32 = h->n - 5;
-        const uint32_t nq = N / 32;
-        poff.resize(nq + 1);
-        for (uint32_t q = 0; q < nq; q++) {
-            poff[q] = (uint32_t)prog.size();
-            gen_prog(ty, ((size_t)1 << n32) + q, 0, false, prog);
-            prog.push_back((uint8_t)OP_END);
-        }
-        poff[nq] = (uint32_t)prog.size();
-        for (int k = 5; k <= h->n && k < 16; k++) {
-            const uint32_t chunk = 1u << (k - 5);
-            uint32_t m = 0;
-            for (uint32_t q = 0; q < nq; q += chunk) m = std::max(m, poff[q + chunk] - poff[q]);
-            h->prog_max[k] = m;
-        }
-        gen_prog(ty, (size_t)1 << n32, 0, true, plain);
-        plain.push_back((uint8_t)OP_END);
-        plain.resize(128, 0);
-        prog.resize(prog.size() + 16, 0);
-    }
     CUDA_TRY(cudaSetDevice(h->device));
     CUDA_TRY(cudaMemcpy(h->d_types, ty.data(), ty.size(), cudaMemcpyHostToDevice));
     CUDA_TRY(cudaMemcpy(h->d_mask, words.data(), words.size() * 4, cudaMemcpyHostToDevice));
-    cudaFree(h->d_prog);
-    cudaFree(h->d_prog_off);
-    cudaFree(h->d_plain_prog);
-    h->d_prog = nullptr;
-    h->d_prog_off = nullptr;
-    h->d_plain_prog = nullptr;
-    if (N >= 32) {
-        CUDA_TRY(cudaMalloc((void **)&h->d_prog, prog.size()));
-        CUDA_TRY(cudaMalloc((void **)&h->d_prog_off, poff.size() * 4));
-        CUDA_TRY(cudaMalloc((void **)&h->d_plain_prog, plain.size()));
-        CUDA_TRY(cudaMemcpy(h->d_prog, prog.data(), prog.size(), cudaMemcpyHostToDevice));
-        CUDA_TRY(cudaMemcpy(h->d_prog_off, poff.data(), poff.size() * 4, cudaMemcpyHostToDevice));
-        CUDA_TRY(cudaMemcpy(h->d_plain_prog, plain.data(), plain.size(), cudaMemcpyHostToDevice));
-    }
     h->have_mask = 1;
     return 0;
 }
@@ -1799,12 +1562,7 @@ static int decode_impl(pq_decoder *h, const float *llr, const uint32_t *ybits, f
     p.X = h->d_x;
     p.dump = dump;
     p.prof = h->profile ? h->d_prof : nullptr;
-    p.prog = h->d_prog;
-    p.prog_off = h->d_prog_off;
-    p.plain_prog = h->d_plain_prog;
-    p.fmask = h->d_mask;
-    p.prog_cap = prog_cap_for(h, p.log2S);
-    const size_t smem = dec_smem_bytes(p.S, p.prog_cap);
+    const size_t smem = dec_smem_bytes(p.S);
     if (h->fmode == PQ_F_MINSUM) {
         CUDA_TRY(cudaFuncSetAttribute(sc_decode_kernel<PQ_F_MINSUM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       (int)smem));
