@@ -533,6 +533,85 @@ __device__ __forceinline__ bool lanes_special(float v, int W, uint32_t t, uint32
     return false;
 }
 
+// ---- frozen-pattern-specialised width-8 nodes.  The polar partial order
+// leaves very few frozen patterns for mixed width-8 nodes (6-10 in the
+// BASELINE codes, covering ~100% of them), so each common pattern gets a
+// straight-line SC routine: no type dispatch, no loops, only shuffles and
+// the f chain.  Rate-1 children are hard decisions behind the same guard as
+// elsewhere; if any guard fails the caller redoes the node generically.
+// Values are lane-distributed (lane i = element i); results are uniform.
+
+// width-4 sub-node, frozen nibble P (bit i = leaf i frozen), lanes 0..3
+template <int FM, uint32_t P>
+__device__ __forceinline__ uint32_t w4_pat(float v, bool &ok)
+{
+    const unsigned FULL = 0xffffffffu;
+    const int lane = threadIdx.x & 31;
+    if constexpr (P == 0xF) {  // rate-0
+        return 0u;
+    } else if constexpr (P == 0x0) {  // rate-1
+        ok &= __all_sync(FULL, lane >= 4 || fabsf(v) >= 5.986585449591075e-08f);  // RATE1_TAU[2]
+        return __ballot_sync(FULL, lane < 4 && v < 0.0f) & 15u;
+    } else if constexpr (P == 0x7) {  // repetition: (L3 + L1) + (L2 + L0), SC's pairing
+        float sum = v + __shfl_down_sync(FULL, v, 2);
+        sum = __shfl_down_sync(FULL, sum, 1) + sum;
+        return __shfl_sync(FULL, sum, 0) < 0.0f ? 15u : 0u;
+    } else if constexpr (P == 0x1) {  // SPC: REP(2) left, rate-1 right
+        const float b = __shfl_down_sync(FULL, v, 2);
+        const float l = pq_f<FM>(v, b);
+        const float l0 = __shfl_sync(FULL, l, 0), l1 = __shfl_sync(FULL, l, 1);
+        const uint32_t u = (l1 + l0) < 0.0f ? 1u : 0u;
+        const float r = pq_g(v, b, u);
+        ok &= __all_sync(FULL, lane >= 2 || fabsf(r) >= 1.5303335787713972e-15f);  // RATE1_TAU[1]
+        const uint32_t xr = __ballot_sync(FULL, lane < 2 && r < 0.0f) & 3u;
+        return ((u ? 3u : 0u) ^ xr) | (xr << 2);
+    } else if constexpr (P == 0x3) {  // rate-0 left, rate-1 right
+        const float r = __shfl_down_sync(FULL, v, 2) + v;
+        ok &= __all_sync(FULL, lane >= 2 || fabsf(r) >= 1.5303335787713972e-15f);
+        const uint32_t xr = __ballot_sync(FULL, lane < 2 && r < 0.0f) & 3u;
+        return xr | (xr << 2);
+    } else {  // P == 0x5: REP(2) left, REP(2) right
+        const float b = __shfl_down_sync(FULL, v, 2);
+        const float l = pq_f<FM>(v, b);
+        const uint32_t u1 = (__shfl_sync(FULL, l, 1) + __shfl_sync(FULL, l, 0)) < 0.0f ? 1u : 0u;
+        const float r = pq_g(v, b, u1);
+        const uint32_t u3 = (__shfl_sync(FULL, r, 1) + __shfl_sync(FULL, r, 0)) < 0.0f ? 1u : 0u;
+        return ((u1 ? 3u : 0u) ^ (u3 ? 3u : 0u)) | ((u3 ? 3u : 0u) << 2);
+    }
+}
+
+template <int FM, uint32_t LP, uint32_t RP>
+__device__ __forceinline__ uint32_t w8_pat(float v, bool &ok)
+{
+    const unsigned FULL = 0xffffffffu;
+    const int lane = threadIdx.x & 31;
+    const float b = __shfl_down_sync(FULL, v, 4);
+    uint32_t xl = 0;
+    if constexpr (LP != 0xF) xl = w4_pat<FM, LP>(pq_f<FM>(v, b), ok);
+    const float r = pq_g(v, b, (xl >> (lane & 3)) & 1u);
+    const uint32_t xr = w4_pat<FM, RP>(r, ok);
+    return (xl ^ xr) | (xr << 4);
+}
+
+// returns true and the bits if the width-8 node's frozen pattern has a routine
+template <int FM>
+__device__ __forceinline__ bool w8_fast(float v, uint32_t pat, uint32_t &bits)
+{
+    bool ok = true;
+    switch (pat) {
+    case 0x01: bits = w8_pat<FM, 0x1, 0x0>(v, ok); break;  // F I I I I I I I
+    case 0x17: bits = w8_pat<FM, 0x7, 0x1>(v, ok); break;  // F F F I F I I I
+    case 0x1F: bits = w8_pat<FM, 0xF, 0x1>(v, ok); break;  // F F F F F I I I
+    case 0x07: bits = w8_pat<FM, 0x7, 0x0>(v, ok); break;  // F F F I I I I I
+    case 0x03: bits = w8_pat<FM, 0x3, 0x0>(v, ok); break;  // F F I I I I I I
+    case 0x3F: bits = w8_pat<FM, 0xF, 0x3>(v, ok); break;  // F F F F F F I I
+    case 0x05: bits = w8_pat<FM, 0x5, 0x0>(v, ok); break;  // F I F I I I I I
+    case 0x15: bits = w8_pat<FM, 0x5, 0x1>(v, ok); break;  // F I F I F I I I
+    default: return false;
+    }
+    return ok;
+}
+
 // W = 8 node, lane i holds element i (lanes 0..7).  One copy (noinline):
 // lane-parallel f/g step, then the width-4 children in registers.
 template <int FM>
@@ -541,6 +620,10 @@ __device__ __noinline__ uint32_t dec8(float v, const TypeBits T, int h, bool pla
     UB_BEGIN();
     const unsigned FULL = 0xffffffffu;
     uint32_t bits;
+    if (!plain && tget(T, h) == NT_MIXED && w8_fast<FM>(v, (T.leaf >> (8 * (h - 4))) & 0xffu, bits)) {
+        UB_END(0);
+        return bits;
+    }
     if (!plain && lanes_special(v, 8, tget(T, h), bits)) {
         UB_END(0);
         return bits;
