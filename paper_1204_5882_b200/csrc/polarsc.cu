@@ -606,7 +606,7 @@ __device__ __forceinline__ uint32_t w8x(float v, bool &ok)
         ok &= __all_sync(FULL, lane >= 8 || fabsf(v) >= 0.00037443434121087193f);  // RATE1_TAU[3]
         return __ballot_sync(FULL, lane < 8 && v < 0.0f) & 0xffu;
     } else {
-        return w8_pat<FM, (P8 & 0xFu), (P8 >> 4)>(v, ok);
+        return w8_pat<FM, P8 & 0xFu, P8 >> 4>(v, ok);
     }
 }
 
