@@ -593,72 +593,6 @@ __device__ __forceinline__ uint32_t w8_pat(float v, bool &ok)
     return (xl ^ xr) | (xr << 4);
 }
 
-// width-8 child of a specialised width-16 node: rate-0 (0xFF), rate-1 (0x00,
-// guarded hard decisions) or a mixed pattern routine
-template <int FM, uint32_t P8>
-__device__ __forceinline__ uint32_t w8x(float v, bool &ok)
-{
-    const unsigned FULL = 0xffffffffu;
-    const int lane = threadIdx.x & 31;
-    if constexpr (P8 == 0xFF) {
-        return 0u;
-    } else if constexpr (P8 == 0x00) {
-        ok &= __all_sync(FULL, lane >= 8 || fabsf(v) >= 0.00037443434121087193f);  // RATE1_TAU[3]
-        return __ballot_sync(FULL, lane < 8 && v < 0.0f) & 0xffu;
-    } else {
-        return w8_pat<FM, P8 & 0xFu, P8 >> 4>(v, ok);
-    }
-}
-
-// width-16 node with left / right width-8 patterns PL, PR (lanes 0..15)
-template <int FM, uint32_t PL, uint32_t PR>
-__device__ __forceinline__ uint32_t w16_pat(float v, bool &ok)
-{
-    const unsigned FULL = 0xffffffffu;
-    const int lane = threadIdx.x & 31;
-    const float b = __shfl_down_sync(FULL, v, 8);
-    uint32_t xl = 0;
-    if constexpr (PL != 0xFF) xl = w8x<FM, PL>(pq_f<FM>(v, b), ok);
-    const float r = pq_g(v, b, (xl >> (lane & 7)) & 1u);
-    const uint32_t xr = w8x<FM, PR>(r, ok);
-    return (xl ^ xr) | (xr << 8);
-}
-
-template <int FM>
-__device__ __noinline__ uint32_t w16_fast(float v, uint32_t pat, int &hit)
-{
-    bool ok = true;
-    uint32_t bits;
-    switch (pat) {
-    case 0x0001: bits = w16_pat<FM, 0x01, 0x00>(v, ok); break;  // SPC16
-    case 0x0117: bits = w16_pat<FM, 0x17, 0x01>(v, ok); break;
-    case 0x177f: bits = w16_pat<FM, 0x7f, 0x17>(v, ok); break;
-    case 0x17ff: bits = w16_pat<FM, 0xff, 0x17>(v, ok); break;
-    case 0x0017: bits = w16_pat<FM, 0x17, 0x00>(v, ok); break;
-    case 0x011f: bits = w16_pat<FM, 0x1f, 0x01>(v, ok); break;
-    case 0x0007: bits = w16_pat<FM, 0x07, 0x00>(v, ok); break;
-    default: hit = 0; return 0u;
-    }
-    hit = ok ? 1 : 0;
-    return bits;
-}
-
-// SPC32: SPC16 left, rate-1 right
-template <int FM>
-__device__ __noinline__ uint32_t w32_spc(float v, int &hit)
-{
-    const unsigned FULL = 0xffffffffu;
-    const int lane = threadIdx.x & 31;
-    bool ok = true;
-    const float b = __shfl_down_sync(FULL, v, 16);
-    const uint32_t xl = w16_pat<FM, 0x01, 0x00>(pq_f<FM>(v, b), ok);
-    const float r = pq_g(v, b, (xl >> (lane & 15)) & 1u);
-    ok &= __all_sync(FULL, lane >= 16 || fabsf(r) >= 0.02961242012679577f);  // RATE1_TAU[4]
-    const uint32_t xr = __ballot_sync(FULL, lane < 16 && r < 0.0f) & 0xffffu;
-    hit = ok ? 1 : 0;
-    return (xl ^ xr) | (xr << 16);
-}
-
 // returns true and the bits if the width-8 node's frozen pattern has a routine
 template <int FM>
 __device__ __forceinline__ bool w8_fast(float v, uint32_t pat, uint32_t &bits)
@@ -717,11 +651,6 @@ __device__ __forceinline__ uint32_t dec16(float v, const TypeBits &T, int h, boo
 {
     const int lane = threadIdx.x & 31;
     uint32_t bits;
-    if (!plain && tget(T, h) == NT_MIXED) {
-        int hit;
-        bits = w16_fast<FM>(v, (T.leaf >> (16 * (h - 2))) & 0xffffu, hit);
-        if (hit) return bits;
-    }
     if (!plain && lanes_special(v, 16, tget(T, h), bits)) return bits;
     const float b = __shfl_down_sync(0xffffffffu, v, 8);
     uint32_t xl = 0, xr = 0;
@@ -753,11 +682,6 @@ __device__ __forceinline__ uint32_t dec32_body(float v, const TypeBits T, bool p
 {
     const int lane = threadIdx.x & 31;
     uint32_t bits;
-    if (!plain && tget(T, 1) == NT_MIXED && T.leaf == 1u) {  // SPC32
-        int hit;
-        bits = w32_spc<FM>(v, hit);
-        if (hit) return bits;
-    }
     if (!plain && lanes_special(v, 32, tget(T, 1), bits)) return bits;
     const float b = __shfl_down_sync(0xffffffffu, v, 16);
     uint32_t xl = 0, xr = 0;
