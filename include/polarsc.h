@@ -53,6 +53,7 @@ extern "C" {
 #define PQ_OPT_SUBTREE_LOG2 2 /* log2 of the shared-memory sub-tree width S; 0 = auto  */
 #define PQ_OPT_FMODE 3        /* PQ_F_EXACT / PQ_F_MINSUM                              */
 #define PQ_OPT_PROFILE 4      /* 1: record per-frame clock64 cycles per step class      */
+#define PQ_OPT_WARP_LOG2 5    /* log2 of the widest node decoded by one warp (5..8, default 8) */
 
 /* slots of the per-frame profile record (pq_decoder_read_profile) */
 #define PQ_PROF_SLOTS 16

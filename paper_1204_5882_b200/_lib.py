@@ -19,6 +19,7 @@ PQ_OPT_SSC = 1
 PQ_OPT_SUBTREE_LOG2 = 2
 PQ_OPT_FMODE = 3
 PQ_OPT_PROFILE = 4
+PQ_OPT_WARP_LOG2 = 5
 PQ_PROF_SLOTS = 16
 PROF_NAMES = ("upper_f", "upper_g", "upper_other", "smem_f", "smem_g", "smem_other", "warp_subtrees",
               "type_staging", "rate1_block", "total", "n_warp_subtrees", "n_block_nodes",

@@ -291,6 +291,7 @@ struct DecParams {
     uint32_t *X;                 // [F][wpf] out: shifted x-hat partial sums
     float *dump;                 // [F][n+1][N] stage dump (plain mode), or null
     unsigned long long *prof;    // [F][PQ_PROF_SLOTS] clock64 cycles per step class, or null
+    uint32_t wmax;               // widest node the single-warp band takes (32..256)
 };
 
 // step classes for the optional per-frame cycle profile (PQ_OPT_PROFILE)
@@ -1015,7 +1016,7 @@ __global__ void __launch_bounds__(256, 2) sc_decode_kernel(DecParams p)
     }
     __syncthreads();
     const int lw = lw_sh;
-    const uint32_t WMAX = S < 256 ? S : 256;  // nodes this wide or narrower: one warp, registers
+    const uint32_t WMAX = S < p.wmax ? S : p.wmax;  // nodes this wide or narrower: one warp
 
     __shared__ unsigned long long eng_prof[4];
     if (tid < 4) eng_prof[tid] = 0;
@@ -1419,6 +1420,7 @@ struct pq_decoder {
     size_t ws_bytes;
     int last_launches;
     int profile;
+    int warp_log2;
     unsigned long long *d_prof;
 };
 
@@ -1467,6 +1469,7 @@ int pq_decoder_create(pq_decoder **out, int n, int max_frames, int f_mode, int d
     h->device = device;
     h->ssc = 1;
     h->log2S_opt = 0;
+    h->warp_log2 = 8;
     h->N = 1u << n;
     h->wpf = h->N >= 32 ? h->N / 32 : 1;
     cudaDeviceProp prop;
@@ -1529,6 +1532,10 @@ int pq_decoder_set_option(pq_decoder *h, int key, int value)
             return set_err(-1, "unknown f mode %d", value);
         h->fmode = value;
         return 0;
+    case PQ_OPT_WARP_LOG2:
+        if (value < 5 || value > 8) return set_err(-1, "warp band log2 width must be in 5..8");
+        h->warp_log2 = value;
+        return 0;
     case PQ_OPT_PROFILE:
         if (value && !h->d_prof) {
             cudaError_t e = cudaMalloc((void **)&h->d_prof, (size_t)h->max_frames * PQ_PROF_SLOTS * 8);
@@ -1558,6 +1565,7 @@ int pq_decoder_get_option(const pq_decoder *h, int key)
     case PQ_OPT_SUBTREE_LOG2: return h->log2S_opt;
     case PQ_OPT_FMODE: return h->fmode;
     case PQ_OPT_PROFILE: return h->profile;
+    case PQ_OPT_WARP_LOG2: return h->warp_log2;
     default: return set_err(-1, "unknown option %d", key);
     }
 }
@@ -1645,6 +1653,7 @@ static int decode_impl(pq_decoder *h, const float *llr, const uint32_t *ybits, f
     p.X = h->d_x;
     p.dump = dump;
     p.prof = h->profile ? h->d_prof : nullptr;
+    p.wmax = 1u << h->warp_log2;
     const size_t smem = dec_smem_bytes(p.S);
     if (h->fmode == PQ_F_MINSUM) {
         CUDA_TRY(cudaFuncSetAttribute(sc_decode_kernel<PQ_F_MINSUM>, cudaFuncAttributeMaxDynamicSharedMemorySize,

@@ -18,6 +18,8 @@ ap = argparse.ArgumentParser()
 ap.add_argument("configs", nargs="*", default=["c1", "c2"])
 ap.add_argument("--frames", type=int, default=0)
 ap.add_argument("--subtree-log2", type=int, default=0)
+ap.add_argument("--warp-log2", type=int, default=8)
+ap.add_argument("--fmode", default="exact")
 a = ap.parse_args()
 dev = torch.device("cuda", 0)
 for key in a.configs:
@@ -26,7 +28,8 @@ for key in a.configs:
     F = a.frames or cfg.frames_per_gpu
     x, llr, _ = gen_frames(cfg, code.block_size, 0, F)
     u = polar_transform_words(torch.from_numpy(pack_bits(x).view(np.int32).copy()).to(dev), code.n)
-    dec = ScDecoder(code, max_frames=F, subtree_log2=a.subtree_log2)
+    dec = ScDecoder(code, max_frames=F, subtree_log2=a.subtree_log2, f_mode=a.fmode)
+    dec.set_option(_lib.PQ_OPT_WARP_LOG2, a.warp_log2)
     l = torch.from_numpy(llr).to(dev)
     dec.decode(l, u)
     dec.set_option(_lib.PQ_OPT_PROFILE, 1)
