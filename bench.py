@@ -171,6 +171,21 @@ def roofline_entry(code, frames, log2S, t_kernel_s, peaks, band_share=None):
     return out
 
 
+def with_traffic(roof, args):
+    """dram read+write bytes per launch from the committed ncu --set full capture
+    of the same config/f mode (profiles/r01/ncu_full_<cfg>.json), if present."""
+    path = os.path.join(ROOT, "profiles", "r01", f"ncu_full_{args.config}.json")
+    try:
+        with open(path) as fh:
+            cap = json.load(fh)
+        if cap.get("fmode") == args.fmode and not args.no_ssc:
+            roof["traffic"] = cap["traffic_bytes_per_launch"]
+            roof["traffic_source"] = os.path.relpath(path, ROOT)
+    except Exception:
+        pass
+    return roof
+
+
 def run_reference(args, rank, world):
     """--impl reference: the reference's decode path has no implementation
     (polar_core is SPEC-only), so the CPU oracle port -- the SPEC restatement --
@@ -376,7 +391,7 @@ def main():
                        "parallelism": f"frames sharded over {world} GPU(s)", "l2": "256 MiB flush between steps"},
             "fer": round(int(stats[0]) / int(stats[1]), 4), "frames_total": int(stats[1]),
             "e2e": e2e, "gpu_launches": launches * args.steps,
-            "roofline": roofline_entry(code, F, log2S, t_kernel, peaks, band_share),
+            "roofline": with_traffic(roofline_entry(code, F, log2S, t_kernel, peaks, band_share), args),
             "kernel_ms": round(1e3 * t_kernel, 3),
             "cpu_baseline": cpu, "clocks": sampler.summary(), "wall_s_timed": round(t_wall, 3),
         }

@@ -21,7 +21,7 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--config", default="c2")
 ap.add_argument("--frames", type=int, default=0)
 ap.add_argument("--reps", type=int, default=2)
-ap.add_argument("--fmode", default="exact")
+ap.add_argument("--fmode", default="fast")
 ap.add_argument("--no-ssc", action="store_true")
 ap.add_argument("--subtree-log2", type=int, default=0)
 a = ap.parse_args()
