@@ -46,6 +46,12 @@ extern "C" {
  * is the north star's tolerance rule against the f64 oracle, not bit-exactness
  * with the fp32 mirror.                                                    */
 #define PQ_F_FAST 2
+/* FIXED: SPEC.md's sc_decode_fixed -- the reference's
+ * default decode path: saturating Q8.8 LLRs (raw = sat(rint(256
+ * L)) of the fp32 channel LLR), f = sgn min(|a|, |b|, phi(sat(phi|a| +
+ * phi|b|))) with the 4096-entry phi table, saturating g.  Integer-exact: the
+ * GPU reproduces the C oracle's decisions and stage values bit for bit.     */
+#define PQ_F_FIXED 3
 
 /* options for pq_decoder_set_option */
 #define PQ_OPT_SSC 1          /* 1 (default): skip rate-0/rate-1/repetition sub-trees

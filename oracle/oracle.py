@@ -63,6 +63,12 @@ def lib():
         L.orc_fmag_f64.argtypes = [ctypes.c_double, ctypes.c_double]
         L.orc_fmag_f64.restype = ctypes.c_double
         L.orc_fmag_f32_vec.argtypes = [f32p, f32p, f32p, ctypes.c_size_t]
+        i16p = np.ctypeslib.ndpointer(np.int16, flags="C_CONTIGUOUS")
+        L.orc_phi_table.argtypes = [i16p]
+        L.orc_quantize.argtypes = [ctypes.c_float]
+        L.orc_quantize.restype = ctypes.c_int16
+        L.orc_sc_decode_fixed.argtypes = [ctypes.c_int, u8p, i16p, u8p, u8p, ctypes.c_void_p, ctypes.c_void_p,
+                                          ctypes.c_void_p]
         L.orc_fmag_f64_vec.argtypes = [f64p, f64p, f64p, ctypes.c_size_t]
         _lib = L
     return _lib
@@ -166,6 +172,43 @@ def sc_decode_batch(mask, llr, frozen_u, precision=64, fmode=F_EXACT, threads=1,
     if rc != 0:
         raise MemoryError("oracle batch decode failed")
     return (out, mi) if min_info else out
+
+
+def phi_table_q88() -> np.ndarray:
+    """The oracle's Q8.8 phi table (4097 entries, index = raw magnitude code)."""
+    out = np.zeros(4097, np.int16)
+    lib().orc_phi_table(out)
+    return out
+
+
+def quantize_q88(llr) -> np.ndarray:
+    """fp32 LLRs -> saturating Q8.8 raw int16 (rint(L * 256), |raw| <= 32767)."""
+    l = np.asarray(llr, np.float32)
+    r = np.rint(l * np.float32(256.0))
+    return np.clip(r, -32767, 32767).astype(np.int16)
+
+
+def sc_decode_fixed(mask, llr_raw, frozen_u, dump=False, leaf=False):
+    """SPEC.md:250-258 fixed-point SC on raw Q8.8 LLRs.  Returns (u, x[, stages][, leaf])."""
+    mask = np.ascontiguousarray(mask, dtype=np.uint8)
+    N = mask.size
+    n = int(np.log2(N))
+    l = np.ascontiguousarray(llr_raw, dtype=np.int16)
+    fz = np.ascontiguousarray(frozen_u, dtype=np.uint8)
+    u = np.empty(N, np.uint8)
+    x = np.empty(N, np.uint8)
+    st = np.zeros((n + 1, N), np.int16) if dump else None
+    lf = np.zeros(N, np.int16) if leaf else None
+    rc = lib().orc_sc_decode_fixed(n, mask, l, fz, u, x.ctypes.data, st.ctypes.data if dump else None,
+                                   lf.ctypes.data if leaf else None)
+    if rc != 0:
+        raise MemoryError("oracle decode failed")
+    out = (u, x)
+    if dump:
+        out += (st,)
+    if leaf:
+        out += (lf,)
+    return out
 
 
 def max_threads() -> int:

@@ -328,6 +328,105 @@ int orc_max_threads(void)
     return c > 0 ? (int)c : 1;
 }
 
+/* ------------------------------------------------------------------------- */
+/* Fixed-point SC: saturating Q8.8 int16 LLRs and the
+ * 4096-entry phi table uniform on (0, 16] (step 2^-8 = one LSB, so the table
+ * index is the raw magnitude code; codes above 4096 use the last entry; phi(0)
+ * saturates; outputs clamped to the representable range).
+ *   f(a, b) = sgn a sgn b min(|a|, |b|, phi(sat(phi|a| + phi|b|)))
+ * The min with |a|, |b| is SURVEY.md App. A.9's fix of the literal rule, which
+ * returns the saturated phi(0) for two large inputs; exact boxplus always
+ * satisfies |f| <= min(|a|, |b|).  g(a, b, s) = sat(b + (1 - 2s) a).
+ * Channel LLRs: raw = sat(rint(L * 256)) of the fp32 LLR (round half even).  */
+
+#define Q_MAX 32767
+static int16_t PHI_TAB[4097];
+static int phi_tab_ready = 0;
+
+void orc_phi_table(int16_t *out)
+{
+    if (!phi_tab_ready) {
+        PHI_TAB[0] = Q_MAX;
+        for (int k = 1; k <= 4096; k++) {
+            double v = -log(tanh((double)k / 512.0)) * 256.0;
+            long r = lrint(v);
+            PHI_TAB[k] = (int16_t)(r > Q_MAX ? Q_MAX : r);
+        }
+        phi_tab_ready = 1;
+    }
+    if (out) memcpy(out, PHI_TAB, sizeof PHI_TAB);
+}
+
+static inline int q_sat(int v) { return v > Q_MAX ? Q_MAX : (v < -Q_MAX ? -Q_MAX : v); }
+static inline int q_phi(int m) { return PHI_TAB[m > 4096 ? 4096 : m]; }
+
+static inline int f_fix(int a, int b)
+{
+    int ma = a < 0 ? -a : a, mb = b < 0 ? -b : b;
+    int s = q_phi(ma) + q_phi(mb);
+    if (s > Q_MAX) s = Q_MAX;
+    int m = q_phi(s);
+    if (ma < m) m = ma;
+    if (mb < m) m = mb;
+    return ((a < 0) != (b < 0)) ? -m : m;
+}
+
+int16_t orc_quantize(float L)
+{
+    float r = rintf(L * 256.0f);
+    if (r > (float)Q_MAX) r = (float)Q_MAX;
+    if (r < -(float)Q_MAX) r = -(float)Q_MAX;
+    return (int16_t)r;
+}
+
+/* llr: N raw Q8.8 values; dump (nullable): (n+1)*N raw stage values */
+int orc_sc_decode_fixed(int n, const uint8_t *mask, const int16_t *llr, const uint8_t *frozen_u,
+                        uint8_t *u_hat, uint8_t *x_hat, int16_t *dump, int16_t *leaf)
+{
+    orc_phi_table(NULL);
+    const size_t N = (size_t)1 << n;
+    int *buf = (int *)malloc(sizeof(int) * 2 * N);
+    uint8_t *xs = (uint8_t *)calloc(N, 1);
+    if (!buf || !xs) { free(buf); free(xs); return -1; }
+    for (size_t i = 0; i < N; i++) buf[i] = q_sat(llr[i]);
+    if (dump) for (size_t i = 0; i < N; i++) dump[i] = (int16_t)buf[i];
+    int d = 0; size_t j = 0; int entering = 1;
+    for (;;) {
+        size_t W = N >> d;
+        if (entering) {
+            if (W == 1) {
+                int L = buf[2 * N - 2];
+                uint8_t u = mask[j] ? (frozen_u[j] & 1) : (uint8_t)(L < 0);
+                if (leaf) leaf[j] = (int16_t)L;
+                u_hat[j] = u; xs[j] = u;
+                entering = 0;
+                continue;
+            }
+            int *nd = buf + (2 * N - 2 * W), *ch = buf + (2 * N - W);
+            for (size_t i = 0; i < W / 2; i++) ch[i] = f_fix(nd[i], nd[i + W / 2]);
+            d++; j = 2 * j;
+            if (dump) for (size_t i = 0; i < W / 2; i++) dump[(size_t)d * N + j * (W / 2) + i] = (int16_t)ch[i];
+            continue;
+        }
+        if (d == 0) break;
+        size_t Wp = W * 2;
+        if ((j & 1) == 0) {
+            int *nd = buf + (2 * N - 2 * Wp), *ch = buf + (2 * N - Wp);
+            const uint8_t *s = xs + j * W;
+            for (size_t i = 0; i < W; i++) ch[i] = q_sat(s[i] ? nd[i + W] - nd[i] : nd[i + W] + nd[i]);
+            j = j + 1; entering = 1;
+            if (dump) for (size_t i = 0; i < W; i++) dump[(size_t)d * N + j * W + i] = (int16_t)ch[i];
+            continue;
+        }
+        uint8_t *xl = xs + (j - 1) * W, *xr = xs + j * W;
+        for (size_t i = 0; i < W; i++) xl[i] ^= xr[i];
+        d--; j >>= 1;
+    }
+    if (x_hat) memcpy(x_hat, xs, N);
+    free(buf); free(xs);
+    return 0;
+}
+
 /* vectorised helpers so tests can pin f itself against the reference form */
 void orc_fmag_f32_vec(const float *a, const float *b, float *out, size_t count)
 {

@@ -11,7 +11,7 @@ from .channel import (LLR_CLAMP, BiAwgn, Bsc, ChannelModel, channel_llr, make_rn
 from .codes import (CONFIGS, PolarCode, available_configs, code_table_checksum, load_config,
                     read_code_table, write_code_table)
 from .polar_core import (ScDecoder, pack_bits, phi, polar_transform, polar_transform_words,
-                         sc_decode, unpack_bits, words_per_frame)
+                         quantize_q88, sc_decode, sc_decode_fixed, unpack_bits, words_per_frame)
 from .reconcile import alice_disclose, bob_decode
 
 __version__ = "0.1.0"
@@ -20,6 +20,7 @@ __all__ = [
     "LLR_CLAMP", "BiAwgn", "Bsc", "ChannelModel", "channel_llr", "make_rng", "transmit",
     "CONFIGS", "PolarCode", "available_configs", "code_table_checksum", "load_config",
     "read_code_table", "write_code_table",
-    "ScDecoder", "pack_bits", "phi", "polar_transform", "polar_transform_words", "sc_decode",
+    "ScDecoder", "pack_bits", "phi", "polar_transform", "polar_transform_words", "quantize_q88",
+    "sc_decode", "sc_decode_fixed",
     "unpack_bits", "words_per_frame", "alice_disclose", "bob_decode", "__version__",
 ]

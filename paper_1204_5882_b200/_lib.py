@@ -15,6 +15,7 @@ LIB_PATH = os.path.join(HERE, "libpolarsc.so")
 PQ_F_EXACT = 0
 PQ_F_MINSUM = 1
 PQ_F_FAST = 2
+PQ_F_FIXED = 3
 PQ_OPT_SSC = 1
 PQ_OPT_SUBTREE_LOG2 = 2
 PQ_OPT_FMODE = 3

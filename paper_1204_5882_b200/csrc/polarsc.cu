@@ -34,6 +34,7 @@
 //    bit for bit.
 
 #include <cuda_runtime.h>
+#include <math.h>
 #include <stdarg.h>
 #include <stdint.h>
 #include <stdio.h>
@@ -243,16 +244,45 @@ __device__ __forceinline__ float pq_fmag_fast(float a, float b)
     return big ? lo - l : l;
 }
 
+
+// g(a, b, s) = b + (1 - 2s) a   (SPEC.md:243)
+__device__ __forceinline__ float pq_g(float a, float b, uint32_t s) { return s ? b - a : b + a; }
+
+// ---- fixed point: Q8.8 raw values carried in fp32
+// registers (integers |r| <= 32767 are exact), saturating adds, phi table.
+#define Q_MAX 32767.0f
+__constant__ short PHI_TAB_C[4097];
+__shared__ short pq_phitab[4097];
+
+template <int FM>
+__device__ __forceinline__ float qadd(float x, float y)
+{
+    const float r = x + y;
+    return FM == PQ_F_FIXED ? fminf(fmaxf(r, -Q_MAX), Q_MAX) : r;
+}
+
+// g with the mode's addition (saturating in fixed point)
+template <int FM>
+__device__ __forceinline__ float pq_gt(float a, float b, uint32_t s) { return qadd<FM>(b, s ? -a : a); }
+
+// f(a, b) = sgn a sgn b min(|a|, |b|, phi(sat(phi|a| + phi|b|))) on raw codes
+__device__ __forceinline__ float pq_fmag_fixed(float a, float b)
+{
+    const int ma = (int)a, mb = (int)b;
+    const int s = min((int)pq_phitab[min(ma, 4096)] + (int)pq_phitab[min(mb, 4096)], 32767);
+    return (float)min(min(ma, mb), (int)pq_phitab[min(s, 4096)]);
+}
+
 template <int FM>
 __device__ __forceinline__ float pq_f(float a, float b)
 {
     const float ma = fabsf(a), mb = fabsf(b);
-    const float mag = FM == PQ_F_MINSUM ? fminf(ma, mb) : (FM == PQ_F_FAST ? pq_fmag_fast(ma, mb) : pq_fmag(ma, mb));
+    const float mag = FM == PQ_F_MINSUM ? fminf(ma, mb)
+                      : FM == PQ_F_FAST ? pq_fmag_fast(ma, mb)
+                      : FM == PQ_F_FIXED ? pq_fmag_fixed(ma, mb)
+                                         : pq_fmag(ma, mb);
     return __uint_as_float(__float_as_uint(mag) | ((__float_as_uint(a) ^ __float_as_uint(b)) & 0x80000000u));
 }
-
-// g(a, b, s) = b + (1 - 2s) a   (SPEC.md:243)
-__device__ __forceinline__ float pq_g(float a, float b, uint32_t s) { return s ? b - a : b + a; }
 
 // Rate-1 shortcut guard.  b(t) = 0.427 t^2 (t < 1), max(0.427, t - ln 2)
 // (t >= 1) lower-bounds |boxplus(t, t)| in exact arithmetic; chained k times
@@ -272,7 +302,16 @@ __constant__ float RATE1_TAU[26] = {
     10.49012279510498f, 11.18332290649414f, 11.8765230178833f, 12.569723129272461f,
     13.262923240661621f, 13.956123352050781f};
 
-__device__ __forceinline__ bool rate1_guard(float m, int k) { return m >= RATE1_TAU[k]; }
+// Fixed-point (Q8.8) counterpart, in raw units: the smallest raw m whose
+// k-fold chain m -> f_fix(m, m) stays >= 1 LSB (f_fix is monotone; computed on
+// the host from the phi table at decoder creation).
+__constant__ float RATE1_TAU_FIX[26];
+
+template <int FM>
+__device__ __forceinline__ float tau(int k) { return FM == PQ_F_FIXED ? RATE1_TAU_FIX[k] : RATE1_TAU[k]; }
+
+template <int FM>
+__device__ __forceinline__ bool rate1_guard(float m, int k) { return m >= tau<FM>(k); }
 
 // ---------------------------------------------------------------------------
 // node types (host computes them from the frozen mask; heap order)
@@ -290,6 +329,7 @@ struct DecParams {
     float *scr;                  // [F][N] stage buffers for widths > S
     uint32_t *X;                 // [F][wpf] out: shifted x-hat partial sums
     float *dump;                 // [F][n+1][N] stage dump (plain mode), or null
+    int fixed;                   // 1: quantise channel LLRs to Q8.8 raw codes on load
     unsigned long long *prof;    // [F][PQ_PROF_SLOTS] clock64 cycles per step class, or null
     uint32_t wmax;               // widest node the single-warp band takes (32..256)
 };
@@ -311,9 +351,10 @@ __device__ __forceinline__ float chan_load(const DecParams &p, const FrameCtx &f
     uint32_t c = fc.cw ? (fc.cw[i >> 5] >> (i & 31)) & 1u : 0u;
     if (fc.y) {
         const uint32_t y = (fc.y[i >> 5] >> (i & 31)) & 1u;
-        return (y ^ c) ? -p.mag : p.mag;
+        return (y ^ c) ? -p.mag : p.mag;  // p.mag is pre-quantised in fixed mode
     }
-    const float v = fc.llr[i];
+    float v = fc.llr[i];
+    if (p.fixed) v = fminf(fmaxf(rintf(v * 256.0f), -Q_MAX), Q_MAX);
     return c ? -v : v;
 }
 
@@ -331,6 +372,12 @@ __device__ __forceinline__ float4 chan_load4(const DecParams &p, const FrameCtx 
         return v;
     }
     v = __ldg(reinterpret_cast<const float4 *>(fc.llr + i));
+    if (p.fixed) {
+        v.x = fminf(fmaxf(rintf(v.x * 256.0f), -Q_MAX), Q_MAX);
+        v.y = fminf(fmaxf(rintf(v.y * 256.0f), -Q_MAX), Q_MAX);
+        v.z = fminf(fmaxf(rintf(v.z * 256.0f), -Q_MAX), Q_MAX);
+        v.w = fminf(fmaxf(rintf(v.w * 256.0f), -Q_MAX), Q_MAX);
+    }
     v.x = __uint_as_float(__float_as_uint(v.x) ^ ((c4 & 1u) << 31));
     v.y = __uint_as_float(__float_as_uint(v.y) ^ ((c4 & 2u) << 30));
     v.z = __uint_as_float(__float_as_uint(v.z) ^ ((c4 & 4u) << 29));
@@ -450,13 +497,13 @@ __device__ __forceinline__ uint32_t dec2(float a, float b, const TypeBits &T, in
 {
     const uint32_t t = plain ? NT_MIXED : tget(T, h);
     if (t == NT_RATE0) return 0u;
-    if (t == NT_REP) return (b + a) < 0.0f ? 3u : 0u;
-    if (t == NT_RATE1 && fminf(fabsf(a), fabsf(b)) >= 1.5303335787713972e-15f)  // RATE1_TAU[1]
+    if (t == NT_REP) return qadd<FM>(b, a) < 0.0f ? 3u : 0u;
+    if (t == NT_RATE1 && fminf(fabsf(a), fabsf(b)) >= tau<FM>(1))
         return (a < 0.0f ? 1u : 0u) | (b < 0.0f ? 2u : 0u);
     const bool fa = (T.leaf >> (2 * h - 32)) & 1u, fb = (T.leaf >> (2 * h - 31)) & 1u;
     const float l = pq_f<FM>(a, b);
     const uint32_t u0 = fa ? 0u : (l < 0.0f ? 1u : 0u);
-    const float r = pq_g(a, b, u0);
+    const float r = pq_gt<FM>(a, b, u0);
     const uint32_t u1 = fb ? 0u : (r < 0.0f ? 1u : 0u);
     if (np.dump && (threadIdx.x & 31) == 0) {
         np.dump[(size_t)(np.d + 1) * np.N + 2 * np.j] = l;
@@ -473,9 +520,9 @@ __device__ __forceinline__ uint32_t dec4(float x0, float x1, float x2, float x3,
 {
     const uint32_t t = plain ? NT_MIXED : tget(T, h);
     if (t == NT_RATE0) return 0u;
-    if (t == NT_REP) return ((x3 + x1) + (x2 + x0)) < 0.0f ? 15u : 0u;
+    if (t == NT_REP) return qadd<FM>(qadd<FM>(x3, x1), qadd<FM>(x2, x0)) < 0.0f ? 15u : 0u;
     if (t == NT_RATE1 &&
-        fminf(fminf(fabsf(x0), fabsf(x1)), fminf(fabsf(x2), fabsf(x3))) >= 5.986585449591075e-08f)  // TAU[2]
+        fminf(fminf(fabsf(x0), fabsf(x1)), fminf(fabsf(x2), fabsf(x3))) >= tau<FM>(2))
         return (x0 < 0.0f ? 1u : 0u) | (x1 < 0.0f ? 2u : 0u) | (x2 < 0.0f ? 4u : 0u) | (x3 < 0.0f ? 8u : 0u);
     uint32_t xl = 0, xr = 0;
     const bool lane0 = (threadIdx.x & 31) == 0;
@@ -488,7 +535,7 @@ __device__ __forceinline__ uint32_t dec4(float x0, float x1, float x2, float x3,
         xl = dec2<FM>(c0, c1, T, 2 * h, plain, child_pos(np, 0));
     }
     if (plain || tget(T, 2 * h + 1) != NT_RATE0) {
-        const float c0 = pq_g(x0, x2, xl & 1u), c1 = pq_g(x1, x3, (xl >> 1) & 1u);
+        const float c0 = pq_gt<FM>(x0, x2, xl & 1u), c1 = pq_gt<FM>(x1, x3, (xl >> 1) & 1u);
         if (np.dump && lane0) {
             np.dump[(size_t)(np.d + 1) * np.N + 4 * np.j + 2] = c0;
             np.dump[(size_t)(np.d + 1) * np.N + 4 * np.j + 3] = c1;
@@ -501,6 +548,7 @@ __device__ __forceinline__ uint32_t dec4(float x0, float x1, float x2, float x3,
 // ---- lane-parallel levels: lane i holds element i of a W = 8 / 16 / 32 node
 
 // rate-1 / repetition handling of a node held one element per lane (lanes < W)
+template <int FM>
 __device__ __forceinline__ bool lanes_special(float v, int W, uint32_t t, uint32_t &bits)
 {
     const unsigned FULL = 0xffffffffu;
@@ -511,7 +559,7 @@ __device__ __forceinline__ bool lanes_special(float v, int W, uint32_t t, uint32
     }
     if (t == NT_RATE1) {
         // both votes issue back to back: guard (all |L| >= tau) and the signs
-        const bool ok = __all_sync(FULL, lane >= W || fabsf(v) >= RATE1_TAU[ilog2((uint32_t)W)]);
+        const bool ok = __all_sync(FULL, lane >= W || fabsf(v) >= tau<FM>(ilog2((uint32_t)W)));
         const uint32_t neg = __ballot_sync(FULL, lane < W && v < 0.0f);
         if (ok) {
             bits = neg & lowmask(W);
@@ -527,7 +575,7 @@ __device__ __forceinline__ bool lanes_special(float v, int W, uint32_t t, uint32
         for (int hh = 16; hh >= 1; hh >>= 1)
             if (hh < W)
 #pragma unroll
-                for (int i = 0; i < hh; i++) x[i] = x[i + hh] + x[i];
+                for (int i = 0; i < hh; i++) x[i] = qadd<FM>(x[i + hh], x[i]);
         bits = x[0] < 0.0f ? lowmask(W) : 0u;
         return true;
     }
@@ -551,32 +599,32 @@ __device__ __forceinline__ uint32_t w4_pat(float v, bool &ok)
     if constexpr (P == 0xF) {  // rate-0
         return 0u;
     } else if constexpr (P == 0x0) {  // rate-1
-        ok &= __all_sync(FULL, lane >= 4 || fabsf(v) >= 5.986585449591075e-08f);  // RATE1_TAU[2]
+        ok &= __all_sync(FULL, lane >= 4 || fabsf(v) >= tau<FM>(2));
         return __ballot_sync(FULL, lane < 4 && v < 0.0f) & 15u;
     } else if constexpr (P == 0x7) {  // repetition: (L3 + L1) + (L2 + L0), SC's pairing
-        float sum = v + __shfl_down_sync(FULL, v, 2);
-        sum = __shfl_down_sync(FULL, sum, 1) + sum;
+        float sum = qadd<FM>(v, __shfl_down_sync(FULL, v, 2));
+        sum = qadd<FM>(__shfl_down_sync(FULL, sum, 1), sum);
         return __shfl_sync(FULL, sum, 0) < 0.0f ? 15u : 0u;
     } else if constexpr (P == 0x1) {  // SPC: REP(2) left, rate-1 right
         const float b = __shfl_down_sync(FULL, v, 2);
         const float l = pq_f<FM>(v, b);
         const float l0 = __shfl_sync(FULL, l, 0), l1 = __shfl_sync(FULL, l, 1);
-        const uint32_t u = (l1 + l0) < 0.0f ? 1u : 0u;
-        const float r = pq_g(v, b, u);
-        ok &= __all_sync(FULL, lane >= 2 || fabsf(r) >= 1.5303335787713972e-15f);  // RATE1_TAU[1]
+        const uint32_t u = qadd<FM>(l1, l0) < 0.0f ? 1u : 0u;
+        const float r = pq_gt<FM>(v, b, u);
+        ok &= __all_sync(FULL, lane >= 2 || fabsf(r) >= tau<FM>(1));
         const uint32_t xr = __ballot_sync(FULL, lane < 2 && r < 0.0f) & 3u;
         return ((u ? 3u : 0u) ^ xr) | (xr << 2);
     } else if constexpr (P == 0x3) {  // rate-0 left, rate-1 right
-        const float r = __shfl_down_sync(FULL, v, 2) + v;
-        ok &= __all_sync(FULL, lane >= 2 || fabsf(r) >= 1.5303335787713972e-15f);
+        const float r = qadd<FM>(__shfl_down_sync(FULL, v, 2), v);
+        ok &= __all_sync(FULL, lane >= 2 || fabsf(r) >= tau<FM>(1));
         const uint32_t xr = __ballot_sync(FULL, lane < 2 && r < 0.0f) & 3u;
         return xr | (xr << 2);
     } else {  // P == 0x5: REP(2) left, REP(2) right
         const float b = __shfl_down_sync(FULL, v, 2);
         const float l = pq_f<FM>(v, b);
-        const uint32_t u1 = (__shfl_sync(FULL, l, 1) + __shfl_sync(FULL, l, 0)) < 0.0f ? 1u : 0u;
-        const float r = pq_g(v, b, u1);
-        const uint32_t u3 = (__shfl_sync(FULL, r, 1) + __shfl_sync(FULL, r, 0)) < 0.0f ? 1u : 0u;
+        const uint32_t u1 = qadd<FM>(__shfl_sync(FULL, l, 1), __shfl_sync(FULL, l, 0)) < 0.0f ? 1u : 0u;
+        const float r = pq_gt<FM>(v, b, u1);
+        const uint32_t u3 = qadd<FM>(__shfl_sync(FULL, r, 1), __shfl_sync(FULL, r, 0)) < 0.0f ? 1u : 0u;
         return ((u1 ? 3u : 0u) ^ (u3 ? 3u : 0u)) | ((u3 ? 3u : 0u) << 2);
     }
 }
@@ -589,7 +637,7 @@ __device__ __forceinline__ uint32_t w8_pat(float v, bool &ok)
     const float b = __shfl_down_sync(FULL, v, 4);
     uint32_t xl = 0;
     if constexpr (LP != 0xF) xl = w4_pat<FM, LP>(pq_f<FM>(v, b), ok);
-    const float r = pq_g(v, b, (xl >> (lane & 3)) & 1u);
+    const float r = pq_gt<FM>(v, b, (xl >> (lane & 3)) & 1u);
     const uint32_t xr = w4_pat<FM, RP>(r, ok);
     return (xl ^ xr) | (xr << 4);
 }
@@ -625,7 +673,7 @@ __device__ __noinline__ uint32_t dec8(float v, const TypeBits T, int h, bool pla
         UB_END(0);
         return bits;
     }
-    if (!plain && lanes_special(v, 8, tget(T, h), bits)) {
+    if (!plain && lanes_special<FM>(v, 8, tget(T, h), bits)) {
         UB_END(0);
         return bits;
     }
@@ -638,7 +686,7 @@ __device__ __noinline__ uint32_t dec8(float v, const TypeBits T, int h, bool pla
                       __shfl_sync(FULL, c, 3), T, 2 * h, plain, child_pos(np, 0));
     }
     if (plain || tget(T, 2 * h + 1) != NT_RATE0) {
-        const float c = pq_g(v, b, (xl >> ((threadIdx.x & 31) & 3)) & 1u);
+        const float c = pq_gt<FM>(v, b, (xl >> ((threadIdx.x & 31) & 3)) & 1u);
         dump_lanes(child_pos(np, 1), c, 4);
         xr = dec4<FM>(__shfl_sync(FULL, c, 0), __shfl_sync(FULL, c, 1), __shfl_sync(FULL, c, 2),
                       __shfl_sync(FULL, c, 3), T, 2 * h + 1, plain, child_pos(np, 1));
@@ -652,7 +700,7 @@ __device__ __forceinline__ uint32_t dec16(float v, const TypeBits &T, int h, boo
 {
     const int lane = threadIdx.x & 31;
     uint32_t bits;
-    if (!plain && lanes_special(v, 16, tget(T, h), bits)) return bits;
+    if (!plain && lanes_special<FM>(v, 16, tget(T, h), bits)) return bits;
     const float b = __shfl_down_sync(0xffffffffu, v, 8);
     uint32_t xl = 0, xr = 0;
     if (plain || tget(T, 2 * h) != NT_RATE0) {
@@ -661,7 +709,7 @@ __device__ __forceinline__ uint32_t dec16(float v, const TypeBits &T, int h, boo
         xl = dec8<FM>(c, T, 2 * h, plain, child_pos(np, 0));
     }
     if (plain || tget(T, 2 * h + 1) != NT_RATE0) {
-        const float c = pq_g(v, b, (xl >> (lane & 7)) & 1u);
+        const float c = pq_gt<FM>(v, b, (xl >> (lane & 7)) & 1u);
         dump_lanes(child_pos(np, 1), c, 8);
         xr = dec8<FM>(c, T, 2 * h + 1, plain, child_pos(np, 1));
     }
@@ -683,7 +731,7 @@ __device__ __forceinline__ uint32_t dec32_body(float v, const TypeBits T, bool p
 {
     const int lane = threadIdx.x & 31;
     uint32_t bits;
-    if (!plain && lanes_special(v, 32, tget(T, 1), bits)) return bits;
+    if (!plain && lanes_special<FM>(v, 32, tget(T, 1), bits)) return bits;
     const float b = __shfl_down_sync(0xffffffffu, v, 16);
     uint32_t xl = 0, xr = 0;
     if (plain || tget(T, 2) != NT_RATE0) {
@@ -692,7 +740,7 @@ __device__ __forceinline__ uint32_t dec32_body(float v, const TypeBits T, bool p
         xl = dec16<FM>(c, T, 2, plain, child_pos(np, 0));
     }
     if (plain || tget(T, 3) != NT_RATE0) {
-        const float c = pq_g(v, b, (xl >> (lane & 15)) & 1u);
+        const float c = pq_gt<FM>(v, b, (xl >> (lane & 15)) & 1u);
         dump_lanes(child_pos(np, 1), c, 16);
         xr = dec16<FM>(c, T, 3, plain, child_pos(np, 1));
     }
@@ -866,7 +914,7 @@ __device__ __noinline__ void warp_walk(float *st_end, uint32_t *xs, const uint8_
                 uint32_t m = 0x7f800000u;
                 for (uint32_t q = 0; q < V; q++) m = min(m, __float_as_uint(nd[32 * q + lane]) & 0x7fffffffu);
                 m = __reduce_min_sync(FULL, m);
-                if (rate1_guard(__uint_as_float(m), ilog2(W))) {
+                if (rate1_guard<FM>(__uint_as_float(m), ilog2(W))) {
                     for (uint32_t q = 0; q < V; q++) {
                         const uint32_t bits = __ballot_sync(FULL, nd[32 * q + lane] < 0.0f);
                         if (lane == 0) xs[(pos >> 5) + q] = bits;
@@ -884,11 +932,11 @@ __device__ __noinline__ void warp_walk(float *st_end, uint32_t *xs, const uint8_
                 for (uint32_t hv = V / 2; hv >= 1; hv >>= 1)
 #pragma unroll
                     for (int q = 0; q < 4; q++)
-                        if (q < (int)hv) sm8[q] = sm8[q + hv] + sm8[q];
+                        if (q < (int)hv) sm8[q] = qadd<FM>(sm8[q + hv], sm8[q]);
                 float s0 = sm8[0];
                 for (int hh = 16; hh >= 1; hh >>= 1) {
                     const float other = __shfl_down_sync(FULL, s0, hh);
-                    s0 = other + s0;
+                    s0 = qadd<FM>(other, s0);
                 }
                 const uint32_t bits = __shfl_sync(FULL, s0, 0) < 0.0f ? FULL : 0u;
                 for (uint32_t w = lane; w < V; w += 32) xs[(pos >> 5) + w] = bits;
@@ -952,7 +1000,7 @@ __device__ __noinline__ void warp_walk(float *st_end, uint32_t *xs, const uint8_
 #pragma unroll
             for (int q = 0; q < 4; q++)
                 if (q < (int)V) {
-                    const float v = pq_g(a[q], b[q], (sw[q] >> lane) & 1u);
+                    const float v = pq_gt<FM>(a[q], b[q], (sw[q] >> lane) & 1u);
                     nd[32 * q + lane] = v;
                     if (dump) dump[(size_t)d * N + (size_t)(j + 1) * W + 32 * q + lane] = v;
                 }
@@ -993,6 +1041,8 @@ __global__ void __launch_bounds__(256, 2) sc_decode_kernel(DecParams p)
     sm.ty = (uint8_t *)(sm.xs + SW);
 
     load_log_table();
+    if (FM == PQ_F_FIXED)
+        for (int i = threadIdx.x; i < 4097; i += blockDim.x) pq_phitab[i] = PHI_TAB_C[i];
     __syncthreads();
     const uint32_t frame = blockIdx.x;
     FrameCtx fc;
@@ -1146,7 +1196,7 @@ __global__ void __launch_bounds__(256, 2) sc_decode_kernel(DecParams p)
                 m = block_min(m, red);
                 int k = 0;
                 for (uint32_t w = W; w > 1; w >>= 1) k++;
-                if (rate1_guard(m, k)) {
+                if (rate1_guard<FM>(m, k)) {
                     uint32_t *xb = xptr(W);
                     const uint32_t base = xpos(W, j * W) >> 5;
                     for (uint32_t i0 = 0; i0 < W; i0 += nthr) {
@@ -1255,10 +1305,10 @@ __global__ void __launch_bounds__(256, 2) sc_decode_kernel(DecParams p)
                     const uint32_t i = base + 4 * (tid + k * nthr);
                     if (i < W) {
                         float4 v;
-                        v.x = pq_g(a[k].x, b[k].x, sb[k] & 1u);
-                        v.y = pq_g(a[k].y, b[k].y, sb[k] & 2u);
-                        v.z = pq_g(a[k].z, b[k].z, sb[k] & 4u);
-                        v.w = pq_g(a[k].w, b[k].w, sb[k] & 8u);
+                        v.x = pq_gt<FM>(a[k].x, b[k].x, sb[k] & 1u);
+                        v.y = pq_gt<FM>(a[k].y, b[k].y, sb[k] & 2u);
+                        v.z = pq_gt<FM>(a[k].z, b[k].z, sb[k] & 4u);
+                        v.w = pq_gt<FM>(a[k].w, b[k].w, sb[k] & 8u);
                         *reinterpret_cast<float4 *>(dst + i) = v;
                         if (dmp) *reinterpret_cast<float4 *>(dmp + i) = v;
                     }
@@ -1354,6 +1404,8 @@ template <int FM>
 __global__ void fmag_kernel(const float *a, const float *b, float *out, int n)
 {
     load_log_table();
+    if (FM == PQ_F_FIXED)
+        for (int i = threadIdx.x; i < 4097; i += blockDim.x) pq_phitab[i] = PHI_TAB_C[i];
     __syncthreads();
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) out[i] = pq_f<FM>(a[i], b[i]);
 }
@@ -1448,6 +1500,54 @@ static size_t dec_smem_bytes(uint32_t S)
     return (size_t)8 * S + (size_t)SW * 4 + (size_t)2 * S;
 }
 
+// Q8.8 phi table and the fixed-point rate-1 thresholds, computed
+// on the host (double-precision libm, rounded to nearest) and uploaded once
+// per device.  oracle/sc_oracle.c builds the same table the same way.
+static void fixed_tables(short *phi, float *tau)
+{
+    phi[0] = 32767;
+    for (int k = 1; k <= 4096; k++) {
+        const long r = lrint(-log(tanh((double)k / 512.0)) * 256.0);
+        phi[k] = (short)(r > 32767 ? 32767 : r);
+    }
+    auto f = [&](int a, int b) {
+        const int s = std::min((int)phi[std::min(a, 4096)] + (int)phi[std::min(b, 4096)], 32767);
+        return std::min(std::min(a, b), (int)phi[std::min(s, 4096)]);
+    };
+    auto chain = [&](int t, int k) {
+        for (int i = 0; i < k; i++) t = f(t, t);
+        return t;
+    };
+    for (int k = 0; k < 26; k++) {
+        if (chain(32767, k) < 1) {
+            tau[k] = 1e30f;  // never take the shortcut
+            continue;
+        }
+        int lo = 0, hi = 32767;  // chain(hi) >= 1; find the smallest such t
+        while (hi - lo > 1) {
+            const int mid = (lo + hi) / 2;
+            if (chain(mid, k) >= 1) hi = mid;
+            else lo = mid;
+        }
+        tau[k] = (float)hi;
+    }
+}
+
+static int ensure_fixed_tables()
+{
+    int dev = 0;
+    CUDA_TRY(cudaGetDevice(&dev));
+    static bool done[64] = {false};
+    if (dev < 64 && done[dev]) return 0;
+    short phi[4097];
+    float tau[26];
+    fixed_tables(phi, tau);
+    CUDA_TRY(cudaMemcpyToSymbol(PHI_TAB_C, phi, sizeof phi));
+    CUDA_TRY(cudaMemcpyToSymbol(RATE1_TAU_FIX, tau, sizeof tau));
+    if (dev < 64) done[dev] = true;
+    return 0;
+}
+
 extern "C" {
 
 const char *pq_last_error(void) { return g_last_error.c_str(); }
@@ -1459,7 +1559,7 @@ int pq_decoder_create(pq_decoder **out, int n, int max_frames, int f_mode, int d
     *out = nullptr;
     if (n < 1 || n > 25) return set_err(-1, "n must be in [1, 25], got %d", n);
     if (max_frames < 1) return set_err(-1, "max_frames must be >= 1, got %d", max_frames);
-    if (f_mode != PQ_F_EXACT && f_mode != PQ_F_MINSUM && f_mode != PQ_F_FAST)
+    if (f_mode != PQ_F_EXACT && f_mode != PQ_F_MINSUM && f_mode != PQ_F_FAST && f_mode != PQ_F_FIXED)
         return set_err(-1, "unknown f mode %d", f_mode);
     CUDA_TRY(cudaSetDevice(device));
     pq_decoder *h = new pq_decoder();
@@ -1528,7 +1628,7 @@ int pq_decoder_set_option(pq_decoder *h, int key, int value)
         h->log2S_opt = value;
         return 0;
     case PQ_OPT_FMODE:
-        if (value != PQ_F_EXACT && value != PQ_F_MINSUM && value != PQ_F_FAST)
+        if (value != PQ_F_EXACT && value != PQ_F_MINSUM && value != PQ_F_FAST && value != PQ_F_FIXED)
             return set_err(-1, "unknown f mode %d", value);
         h->fmode = value;
         return 0;
@@ -1654,8 +1754,18 @@ static int decode_impl(pq_decoder *h, const float *llr, const uint32_t *ybits, f
     p.dump = dump;
     p.prof = h->profile ? h->d_prof : nullptr;
     p.wmax = 1u << h->warp_log2;
+    p.fixed = h->fmode == PQ_F_FIXED ? 1 : 0;
+    if (p.fixed) {
+        int rc = ensure_fixed_tables();
+        if (rc) return rc;
+        p.mag = fminf(fmaxf(rintf(mag * 256.0f), -32767.0f), 32767.0f);
+    }
     const size_t smem = dec_smem_bytes(p.S);
-    if (h->fmode == PQ_F_MINSUM) {
+    if (h->fmode == PQ_F_FIXED) {
+        CUDA_TRY(cudaFuncSetAttribute(sc_decode_kernel<PQ_F_FIXED>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)smem));
+        sc_decode_kernel<PQ_F_FIXED><<<frames, 256, smem, st>>>(p);
+    } else if (h->fmode == PQ_F_MINSUM) {
         CUDA_TRY(cudaFuncSetAttribute(sc_decode_kernel<PQ_F_MINSUM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       (int)smem));
         sc_decode_kernel<PQ_F_MINSUM><<<frames, 256, smem, st>>>(p);
@@ -1727,6 +1837,12 @@ int pq_debug_fmag(int f_mode, const float *a, const float *b, float *out, int n,
     switch (f_mode) {
     case PQ_F_EXACT: fmag_kernel<PQ_F_EXACT><<<grid, 256, 0, st>>>(a, b, out, n); break;
     case PQ_F_MINSUM: fmag_kernel<PQ_F_MINSUM><<<grid, 256, 0, st>>>(a, b, out, n); break;
+    case PQ_F_FIXED: {
+        int rc = ensure_fixed_tables();
+        if (rc) return rc;
+        fmag_kernel<PQ_F_FIXED><<<grid, 256, 0, st>>>(a, b, out, n);
+        break;
+    }
     case PQ_F_FAST: fmag_kernel<PQ_F_FAST><<<grid, 256, 0, st>>>(a, b, out, n); break;
     default: return set_err(-1, "unknown f mode %d", f_mode);
     }

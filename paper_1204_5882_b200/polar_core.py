@@ -99,7 +99,7 @@ def _check_words(t, frames, wpf, name):
 
 
 F_MODES = {"exact": _lib.PQ_F_EXACT, "fast": _lib.PQ_F_FAST, "min-sum": _lib.PQ_F_MINSUM,
-           "minsum": _lib.PQ_F_MINSUM}
+           "minsum": _lib.PQ_F_MINSUM, "fixed": _lib.PQ_F_FIXED}
 
 
 class ScDecoder:
@@ -111,7 +111,7 @@ class ScDecoder:
                  ssc: bool = True, subtree_log2: int = 0, device=None):
         self.device = _require_cuda(device)
         if f_mode not in F_MODES:
-            raise ValueError(f"unknown f mode {f_mode!r} (exact | fast | min-sum)")
+            raise ValueError(f"unknown f mode {f_mode!r} (exact | fast | fixed | min-sum)")
         L = _lib.load()
         self.code = code
         self.n = code.n
@@ -285,6 +285,24 @@ def scatter_frozen_values(code: PolarCode, frozen_values) -> np.ndarray:
     full = np.zeros(fv.shape[:-1] + (code.block_size,), np.uint8)
     full[..., fi] = fv & 1
     return full
+
+
+def quantize_q88(llrs) -> np.ndarray:
+    """LLRs -> saturating Q8.8 raw codes (int16): sat(rint(256 * fp32(L))), the
+    representation of SPEC.md:207-212 / :269 that sc_decode_fixed consumes."""
+    l = np.asarray(llrs, dtype=np.float32)
+    return np.clip(np.rint(l * np.float32(256.0)), -32767, 32767).astype(np.int16)
+
+
+def sc_decode_fixed(code: PolarCode, llrs_fixed, frozen_values) -> np.ndarray:
+    """SC decode of raw Q8.8 LLRs (int16 codes) with saturating
+    fixed-point arithmetic and the phi table, on the GPU (bit-exact with the
+    fixed-point oracle).  Raw codes travel as fp32 raw/256 (exact) and are
+    re-quantised exactly on load."""
+    raw = np.asarray(llrs_fixed)
+    if raw.dtype.kind not in "iu":
+        raise ValueError("llrs_fixed must be integer Q8.8 codes (see quantize_q88)")
+    return sc_decode(code, raw.astype(np.float32) / np.float32(256.0), frozen_values, f_mode="fixed")
 
 
 def sc_decode(code: PolarCode, llrs, frozen_values, f_mode: str = "exact") -> np.ndarray:

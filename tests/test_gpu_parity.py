@@ -367,3 +367,118 @@ def test_stage_llrs_fast_within_tolerance(cuda, n):
             assert np.array_equal(u[f], u64)
             got = dump[f].astype(np.float64) * sign
             assert np.all(np.abs(got - st64) <= 1e-4 * np.abs(st64) + 1e-6)
+
+
+# --------------------------------------------------------------------------
+# fixed point: SPEC.md's sc_decode_fixed (Q8.8, phi table) -- integer exact
+
+def fix_f_numpy(a, b, tab):
+    ma, mb = np.abs(a).astype(np.int64), np.abs(b).astype(np.int64)
+    s = np.minimum(tab[np.minimum(ma, 4096)].astype(np.int64) + tab[np.minimum(mb, 4096)], 32767)
+    m = np.minimum(np.minimum(ma, mb), tab[np.minimum(s, 4096)])
+    return np.where((a < 0) != (b < 0), -m, m)
+
+
+def test_fixed_f_matches_oracle_table(cuda):
+    import torch
+    from paper_1204_5882_b200.polar_core import f_device
+    tab = O.phi_table_q88()
+    assert abs(tab[512] / 256.0 - O.phi(2.0)) <= 2 ** -7
+    rng = np.random.default_rng(21)
+    a = rng.integers(-32767, 32768, 500000).astype(np.float32)
+    b = np.where(rng.random(a.size) < 0.5, rng.integers(-600, 601, a.size),
+                 rng.integers(-32767, 32768, a.size)).astype(np.float32)
+    got = f_device(torch.from_numpy(a).to(cuda), torch.from_numpy(b).to(cuda), "fixed").cpu().numpy()
+    ref = fix_f_numpy(a.astype(np.int64), b.astype(np.int64), tab)
+    assert np.array_equal(got.astype(np.int64), ref)
+
+
+def fixed_oracle_batch(code, raw, fz):
+    return np.array([O.sc_decode_fixed(code.frozen_mask, raw[f], fz[f])[0] for f in range(raw.shape[0])])
+
+
+@pytest.mark.parametrize("n", [3, 4, 8, 12, 16])
+@pytest.mark.parametrize("ssc", [True, False])
+def test_fixed_random_codes_bit_exact(cuda, n, ssc):
+    rng = np.random.default_rng(300 + n)
+    code = random_code(n, 0.45, rng)
+    F, N = (8 if n < 16 else 3), 1 << n
+    llr = rng.normal(0.8, 1.8, (F, N)).astype(np.float32)
+    llr[:, rng.integers(0, N, 3)] = 0.0
+    fz = rng.integers(0, 2, (F, N)).astype(np.uint8)
+    raw = O.quantize_q88(llr)
+    ref = fixed_oracle_batch(code, raw, fz)
+    u, _ = gpu_decode(cuda, code, llr, fz, ssc=ssc, fmode="fixed")
+    assert np.array_equal(u, ref)
+
+
+@pytest.mark.parametrize("n", [3, 7, 11])
+def test_fixed_stage_dump_bit_exact(cuda, n):
+    rng = np.random.default_rng(400 + n)
+    code = random_code(n, 0.45, rng)
+    F, N = 4, 1 << n
+    llr = rng.normal(0.8, 1.8, (F, N)).astype(np.float32)
+    fz = rng.integers(0, 2, (F, N)).astype(np.uint8)
+    dec = ScDecoder(code, max_frames=F, f_mode="fixed")
+    u, _, dump = dec.decode_dump(to_dev(llr, cuda), words_dev(fz, cuda))
+    dump = dump.cpu().numpy()
+    raw = O.quantize_q88(llr)
+    for f in range(F):
+        sign = 1 - 2 * node_flips(code.frozen_mask, fz[f], n).astype(np.int64)
+        uo, _, st = O.sc_decode_fixed(code.frozen_mask, raw[f], fz[f], dump=True)
+        assert np.array_equal(dump[f].astype(np.int64) * sign, st.astype(np.int64))
+
+
+@pytest.mark.parametrize("key", list(K.CONFIGS))
+def test_config_parity_fixed(cuda, key):
+    if key not in K.available_configs():
+        pytest.skip(f"{key}.pqct not built")
+    frames = {"c1": 64, "c2": 16, "c3": 6, "c4": 6, "c5": 1}[key]
+    cfg, code, x, u_true, llr = config_batch(key, frames)
+    ref = fixed_oracle_batch(code, O.quantize_q88(llr), u_true)
+    u, xh = gpu_decode(cuda, code, llr, u_true, fmode="fixed")
+    assert np.array_equal(u, ref)
+    assert np.array_equal(np.all(u == u_true, axis=1), np.all(xh == x, axis=1))
+
+
+def test_fixed_bsc_front_end_matches(cuda):
+    if "c1" not in K.available_configs():
+        pytest.skip("c1 not built")
+    cfg, code, x, u_true, llr = config_batch("c1", 64)
+    y = np.array([C.frame(cfg.channel, cfg.seed, j, code.block_size)[1] for j in range(64)])
+    dec = ScDecoder(code, max_frames=64, f_mode="fixed")
+    u1, _ = dec.decode(to_dev(llr, cuda), words_dev(u_true, cuda))
+    u2, _ = dec.decode_bsc(words_dev(y, cuda), np.float32(cfg.channel.llr_magnitude), words_dev(u_true, cuda))
+    assert np.array_equal(u1.cpu().numpy(), u2.cpu().numpy())
+
+
+def test_fixed_spec_examples(cuda):
+    """noiseless exactness; on the Table-1 row-1 code (BSC 2%,
+    N=2^16, FER-0.1 frozen set) 500 frames: >= 98% frame agreement with the
+    float decoder and fixed FER <= 2x float FER."""
+    from paper_1204_5882_b200.polar_core import sc_decode_fixed, quantize_q88
+    rng = np.random.default_rng(12)
+    code = random_code(10, 0.3, rng)
+    x = rng.integers(0, 2, 1024).astype(np.uint8)
+    u = O.polar_transform_bytes(x)
+    got = sc_decode_fixed(code, quantize_q88((1.0 - 2.0 * x) * 30.0), u[code.frozen_indices()])
+    assert np.array_equal(got, u)
+    import os
+    path = os.path.join(K.CODES_DIR, "t1r1.pqct")
+    if not os.path.exists(path):
+        pytest.skip("t1r1.pqct not built")
+    code = K.read_code_table(path)
+    ch, seed, F = C.Bsc(0.02), 4242, 500
+    xs, ls = [], []
+    for j in range(F):
+        xj, yj = C.frame(ch, seed, j, code.block_size)
+        xs.append(xj)
+        ls.append(C.channel_llr(ch, yj).astype(np.float32))
+    llr = np.array(ls)
+    uu = np.array([O.polar_transform_bytes(xj) for xj in xs])
+    u_fix, _ = gpu_decode(cuda, code, llr, uu, fmode="fixed")
+    u_flt, _ = gpu_decode(cuda, code, llr, uu, fmode="exact")
+    ok_fix, ok_flt = np.all(u_fix == uu, axis=1), np.all(u_flt == uu, axis=1)
+    agree = np.mean(np.all(u_fix == u_flt, axis=1))
+    assert agree >= 0.98
+    assert (1 - ok_fix.mean()) <= 2 * (1 - ok_flt.mean()) + 1e-12
