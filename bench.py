@@ -44,7 +44,7 @@ def parse():
     ap.add_argument("--config", default="c3")
     ap.add_argument("--frames", type=int, default=0, help="frames per GPU (default: the config's)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--fmode", default="fast", choices=["exact", "fast", "min-sum"])
+    ap.add_argument("--fmode", default="fast", choices=["exact", "fast", "fixed", "min-sum"])
     ap.add_argument("--no-ssc", action="store_true")
     ap.add_argument("--cpu-sample-s", type=float, default=10.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -384,7 +384,7 @@ def main():
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 3),
             "higher_is_better": True, "scaling": "weak",
             "vs_baseline": round(value / PAPER_MBPS[args.config], 1) if args.config in PAPER_MBPS else None,
-            "dtype": {"exact": "f32", "fast": "f32 (SFU transcendentals)", "min-sum": "f32-minsum"}[args.fmode],
+            "dtype": {"exact": "f32", "fast": "f32 (SFU transcendentals)", "fixed": "q8.8 (saturating int16 semantics)", "min-sum": "f32-minsum"}[args.fmode],
             "data": "synthetic: reference channel model, seeded (SURVEY 8(d)); reference-constructed frozen set",
             "config": {"workload": cfg.desc, "key": args.config, "frames_per_gpu": F, "N": N,
                        "rate": cfg.rate, "f": args.fmode, "ssc": not args.no_ssc, "subtree_log2": log2S,
