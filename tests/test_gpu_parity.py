@@ -482,3 +482,32 @@ def test_fixed_spec_examples(cuda):
     agree = np.mean(np.all(u_fix == u_flt, axis=1))
     assert agree >= 0.98
     assert (1 - ok_fix.mean()) <= 2 * (1 - ok_flt.mean()) + 1e-12
+
+
+@pytest.mark.parametrize("rep", ["float", "fixed"])
+def test_run_trials_counts_match_oracle(cuda, rep):
+    """trials.run_trials: the GPU's discarded-frame count
+    equals the oracle's on the same seeded frames (c1, 96 trials, batch 40 so
+    the last batch is ragged)."""
+    from paper_1204_5882_b200.trials import run_trials
+    if "c1" not in K.available_configs():
+        pytest.skip("c1 not built")
+    cfg = K.CONFIGS["c1"]
+    code = K.load_config("c1")
+    T, N, seed = 96, code.block_size, 77
+    xs, llrs = [], []
+    for j in range(T):
+        x, y = C.frame(cfg.channel, seed, j, N)
+        xs.append(x)
+        llrs.append(C.channel_llr(cfg.channel, y))
+    xs, llrs = np.array(xs), np.array(llrs, np.float32)
+    u_true = transform_rows(xs)
+    if rep == "fixed":
+        u = fixed_oracle_batch(code, O.quantize_q88(llrs), u_true)
+    else:
+        u = np.array([O.sc_decode(code.frozen_mask, llrs[t], u_true[t], precision=32)[0] for t in range(T)])
+    expect = int(np.sum(np.any(u != u_true, axis=1)))
+    row = run_trials(code, cfg.channel, T, seed, representation=rep, batch=40, device=cuda)
+    assert row.trials == T and row.n == code.n
+    assert row.fer_measured == expect / T
+    assert row.throughput_mbps > 0
