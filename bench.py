@@ -44,7 +44,7 @@ def parse():
     ap.add_argument("--config", default="c3")
     ap.add_argument("--frames", type=int, default=0, help="frames per GPU (default: the config's)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--fmode", default="fast", choices=["exact", "fast", "fixed", "min-sum"])
+    ap.add_argument("--fmode", default="fixed", choices=["exact", "fast", "fixed", "min-sum"])
     ap.add_argument("--no-ssc", action="store_true")
     ap.add_argument("--cpu-sample-s", type=float, default=10.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -126,9 +126,16 @@ class ClockSampler:
                 "samples": len(self.samples)}
 
 
-def cpu_baseline(code, llr, u, sample_s, threads=1):
-    """The oracle port (f64 exact SC, SPEC restatement) on host cores: decode
-    frames until ~sample_s of CPU work; Mbit/s of block bits."""
+def oracle_precision(fmode):
+    """The CPU decoder timed beside an f mode: the Q8.8 fixed-point port for
+    --fmode fixed (the paper's Table-1 technique), else the
+    f64 exact SC port."""
+    return (16, "Q8.8 fixed-point SC (phi table)") if fmode == "fixed" else (64, "f64 exact SC")
+
+
+def cpu_baseline(code, llr, u, sample_s, threads=1, precision=64):
+    """The oracle port (SPEC restatement) on host cores: decode frames until
+    ~sample_s of CPU work; Mbit/s of block bits."""
     from oracle import oracle as O
 
     N = code.block_size
@@ -137,7 +144,7 @@ def cpu_baseline(code, llr, u, sample_s, threads=1):
     while True:
         k = min(threads, F - (done % F))
         idx = [(done + i) % F for i in range(k)]
-        O.sc_decode_batch(code.frozen_mask, llr[idx], u[idx], precision=64, threads=threads)
+        O.sc_decode_batch(code.frozen_mask, llr[idx], u[idx], precision=precision, threads=threads)
         done += k
         el = time.perf_counter() - t0
         if el >= sample_s or done >= 4 * F:
@@ -145,22 +152,25 @@ def cpu_baseline(code, llr, u, sample_s, threads=1):
     return done * N / el / 1e6, done, el
 
 
-def roofline_entry(code, frames, log2S, t_kernel_s, peaks, band_share=None):
+def roofline_entry(code, frames, log2S, t_kernel_s, peaks, band_share=None, fmode="fast"):
     """Dominant kernel: sc_decode_kernel.  Algorithmic bytes per launch =
     SURVEY.md 8(d)'s 12.3125 N bytes per HBM-streamed level per frame x the
     levels this launch streams through the per-frame scratch (n - log2 S).
+    (int16 stage storage for the fixed-point mode halves those bytes but
+    measured slower: the per-frame streams are latency-bound, not byte-bound.)
     `achieved` divides them by the whole kernel time; `upper_band` divides
     them by the kernel time spent in the upper band (its share of the per-frame
     cycle profile, frames run concurrently), which is what the north star's
     ">= 50% of the binding roofline on the upper stages" refers to."""
     n = code.n
     L_up = max(0, n - log2S)
-    alg = 12.3125 * code.block_size * frames * L_up
+    eb = 4  # stage LLRs are fp32 in every f mode (Q8.8 codes are exact in fp32)
+    alg = (3 * eb + 0.3125) * L_up * code.block_size * frames
     peak = peaks.get("hbm_gbs", 6650.0)
     achieved = alg / t_kernel_s / 1e9 if t_kernel_s > 0 else 0.0
     out = {"bound": "hbm", "achieved": round(achieved, 2), "peak": peak, "unit": "GB/s",
            "frac": round(achieved / peak, 4), "traffic": None,
-           "kernel": "sc_decode_kernel", "alg_bytes_per_launch": alg, "upper_levels": L_up,
+           "kernel": "sc_decode_kernel", "alg_bytes_per_launch": alg, "upper_levels": L_up, "stage_bytes_per_llr": eb,
            "peak_source": "MEASURED_PEAKS.json" if "hbm_gbs" in peaks else "fallback B200_PROFILING.md"}
     if band_share and band_share.get("upper", 0) > 0 and L_up > 0:
         t_up = band_share["upper"] * t_kernel_s
@@ -202,10 +212,11 @@ def run_reference(args, rank, world):
     F = threads
     x, llr, _ = gen_frames(cfg, N, 0, F)
     u = np.array([O.polar_transform_bytes(xi) for xi in x])
+    prec, what = oracle_precision(args.fmode)
     times = []
     for s in range(args.warmup + args.steps):
         t0 = time.perf_counter()
-        O.sc_decode_batch(code.frozen_mask, llr, u, precision=64, threads=threads)
+        O.sc_decode_batch(code.frozen_mask, llr, u, precision=prec, threads=threads)
         dt = time.perf_counter() - t0
         if s >= args.warmup:
             times.append(dt)
@@ -213,11 +224,12 @@ def run_reference(args, rank, world):
     v = F * N * len(times) / tot / 1e6
     line = {"metric": "SC-decoded Mbit/s", "value": round(v, 3), "unit": "Mbit/s", "n_gpus": 0,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(1e3 * tot / len(times), 3),
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "q8.8 (int16)" if prec == 16 else "f64",
             "data": "synthetic (reference channel model, seeded)", "impl": "reference",
-            "config": {"workload": cfg.desc, "key": args.config, "frames_per_step": F, "N": N},
+            "config": {"workload": cfg.desc, "key": args.config, "frames_per_step": F, "N": N, "f": args.fmode},
             "cpu_baseline": {"value": round(v, 3), "unit": "Mbit/s", "cores": threads, "kind": "port",
-                             "sample": f"{F} frames of {args.config} per step (one per thread), f64 exact SC"},
+                             "sample": f"{F} frames of {args.config} per step (one per thread), {what}"},
             "e2e": {"value": round(v, 3), "unit": "Mbit/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -376,9 +388,10 @@ def main():
         if not args.no_cpu_baseline:
             from oracle import oracle as O
             u_np = np.array([O.polar_transform_bytes(xi) for xi in x[:8]])
-            v, nfr, el = cpu_baseline(code, llr[:8], u_np, args.cpu_sample_s, threads=1)
+            prec, what = oracle_precision(args.fmode)
+            v, nfr, el = cpu_baseline(code, llr[:8], u_np, args.cpu_sample_s, threads=1, precision=prec)
             cpu = {"value": round(v, 3), "unit": "Mbit/s", "cores": 1, "kind": "port",
-                   "sample": f"{nfr} frames of {args.config} (N=2^{n}) in {el:.1f} s, f64 exact SC, 1 thread"}
+                   "sample": f"{nfr} frames of {args.config} (N=2^{n}) in {el:.1f} s, {what}, 1 thread"}
         line = {
             "metric": "SC-decoded Mbit/s", "value": round(value, 2), "unit": "Mbit/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 3),
@@ -391,7 +404,7 @@ def main():
                        "parallelism": f"frames sharded over {world} GPU(s)", "l2": "256 MiB flush between steps"},
             "fer": round(int(stats[0]) / int(stats[1]), 4), "frames_total": int(stats[1]),
             "e2e": e2e, "gpu_launches": launches * args.steps,
-            "roofline": with_traffic(roofline_entry(code, F, log2S, t_kernel, peaks, band_share), args),
+            "roofline": with_traffic(roofline_entry(code, F, log2S, t_kernel, peaks, band_share, args.fmode), args),
             "kernel_ms": round(1e3 * t_kernel, 3),
             "cpu_baseline": cpu, "clocks": sampler.summary(), "wall_s_timed": round(t_wall, 3),
         }

@@ -65,6 +65,7 @@ def lib():
         L.orc_fmag_f32_vec.argtypes = [f32p, f32p, f32p, ctypes.c_size_t]
         i16p = np.ctypeslib.ndpointer(np.int16, flags="C_CONTIGUOUS")
         L.orc_phi_table.argtypes = [i16p]
+        L.orc_corr_table.argtypes = [i16p]
         L.orc_quantize.argtypes = [ctypes.c_float]
         L.orc_quantize.restype = ctypes.c_int16
         L.orc_sc_decode_fixed.argtypes = [ctypes.c_int, u8p, i16p, u8p, u8p, ctypes.c_void_p, ctypes.c_void_p,
@@ -172,6 +173,13 @@ def sc_decode_batch(mask, llr, frozen_u, precision=64, fmode=F_EXACT, threads=1,
     if rc != 0:
         raise MemoryError("oracle batch decode failed")
     return (out, mi) if min_info else out
+
+
+def corr_table_q88() -> np.ndarray:
+    """The fixed-point f's table: CORR[k] = rint(256 ln(1 + e^(-k/256))), k = 0..4096."""
+    out = np.zeros(4097, np.int16)
+    lib().orc_corr_table(out)
+    return out
 
 
 def phi_table_q88() -> np.ndarray:

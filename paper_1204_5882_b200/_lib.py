@@ -10,7 +10,8 @@ import ctypes
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libpolarsc.so")
+# PQ_LIB_PATH: an alternative build of the same library (kernel A/B experiments)
+LIB_PATH = os.environ.get("PQ_LIB_PATH") or os.path.join(HERE, "libpolarsc.so")
 
 PQ_F_EXACT = 0
 PQ_F_MINSUM = 1

@@ -41,6 +41,8 @@
 #include <stdlib.h>
 #include <string.h>
 
+#include <algorithm>
+#include <climits>
 #include <string>
 #include <vector>
 
@@ -249,10 +251,14 @@ __device__ __forceinline__ float pq_fmag_fast(float a, float b)
 __device__ __forceinline__ float pq_g(float a, float b, uint32_t s) { return s ? b - a : b + a; }
 
 // ---- fixed point: Q8.8 raw values carried in fp32
-// registers (integers |r| <= 32767 are exact), saturating adds, phi table.
+// registers (integers |r| <= 32767 are exact), saturating adds, and the exact
+// boxplus by table lookup (oracle/sc_oracle.c explains the choice of table):
+//   |f| = max(0, min(|a|, |b|) + CORR[min(|a| + |b|, 4096)] - CORR[min(||a| - |b||, 4096)])
+// CORR[k] = rint(256 ln(1 + e^(-k/256))) held as fp32 in shared memory (no
+// int/float conversions; the two lookups are independent).
 #define Q_MAX 32767.0f
-__constant__ short PHI_TAB_C[4097];
-__shared__ short pq_phitab[4097];
+__constant__ float CORR_TAB_C[4097];
+__shared__ float pq_corrtab[4097];
 
 template <int FM>
 __device__ __forceinline__ float qadd(float x, float y)
@@ -265,12 +271,15 @@ __device__ __forceinline__ float qadd(float x, float y)
 template <int FM>
 __device__ __forceinline__ float pq_gt(float a, float b, uint32_t s) { return qadd<FM>(b, s ? -a : a); }
 
-// f(a, b) = sgn a sgn b min(|a|, |b|, phi(sat(phi|a| + phi|b|))) on raw codes
-__device__ __forceinline__ float pq_fmag_fixed(float a, float b)
+// exact small integer held in a float -> int, with full-rate ALU ops
+__device__ __forceinline__ int small_f2i(float x) { return __float_as_int(x + 12582912.0f) - 0x4B400000; }
+
+// magnitudes ma, mb (raw codes)
+__device__ __forceinline__ float pq_fmag_fixed(float ma, float mb)
 {
-    const int ma = (int)a, mb = (int)b;
-    const int s = min((int)pq_phitab[min(ma, 4096)] + (int)pq_phitab[min(mb, 4096)], 32767);
-    return (float)min(min(ma, mb), (int)pq_phitab[min(s, 4096)]);
+    const int is = small_f2i(fminf(ma + mb, 4096.0f));
+    const int id = small_f2i(fminf(fabsf(ma - mb), 4096.0f));
+    return fmaxf(fminf(ma, mb) + pq_corrtab[is] - pq_corrtab[id], 0.0f);
 }
 
 template <int FM>
@@ -302,9 +311,10 @@ __constant__ float RATE1_TAU[26] = {
     10.49012279510498f, 11.18332290649414f, 11.8765230178833f, 12.569723129272461f,
     13.262923240661621f, 13.956123352050781f};
 
-// Fixed-point (Q8.8) counterpart, in raw units: the smallest raw m whose
-// k-fold chain m -> f_fix(m, m) stays >= 1 LSB (f_fix is monotone; computed on
-// the host from the phi table at decoder creation).
+// Fixed-point (Q8.8) counterpart, in raw units: L(t) = min over a, b >= t of
+// |f_fix(a, b)| (a suffix minimum, so non-decreasing); RATE1_TAU_FIX[k] is the
+// smallest raw m whose k-fold chain m -> L(m) stays >= 1 LSB.  Computed on the
+// host from the table at first use (fixed_tables).
 __constant__ float RATE1_TAU_FIX[26];
 
 template <int FM>
@@ -1042,7 +1052,7 @@ __global__ void __launch_bounds__(256, 2) sc_decode_kernel(DecParams p)
 
     load_log_table();
     if (FM == PQ_F_FIXED)
-        for (int i = threadIdx.x; i < 4097; i += blockDim.x) pq_phitab[i] = PHI_TAB_C[i];
+        for (int i = threadIdx.x; i < 4097; i += blockDim.x) pq_corrtab[i] = CORR_TAB_C[i];
     __syncthreads();
     const uint32_t frame = blockIdx.x;
     FrameCtx fc;
@@ -1225,8 +1235,34 @@ __global__ void __launch_bounds__(256, 2) sc_decode_kernel(DecParams p)
             float *dst = stage_ptr(p, fc, sm, H);
             float *dmp = fc.dump ? fc.dump + (size_t)(d + 1) * N + (size_t)(2 * j) * H : nullptr;
             // f-step, 4 consecutive elements per thread (H >= 256 here, so every
-            // chunk is a whole float4); the f's arithmetic hides the load latency
+            // chunk is a whole float4)
             const bool ch0 = d == 0;
+            if (!ch0 && W > S && H % (8 * nthr) == 0) {
+                // from HBM/L2: two chunks per thread in flight
+#pragma unroll 1
+                for (uint32_t i = 4 * tid; i < H; i += 8 * nthr) {
+                    const uint32_t i2 = i + 4 * nthr;
+                    const float4 a = *reinterpret_cast<const float4 *>(src + i);
+                    const float4 b = *reinterpret_cast<const float4 *>(src + i + H);
+                    const float4 a2 = *reinterpret_cast<const float4 *>(src + i2);
+                    const float4 b2 = *reinterpret_cast<const float4 *>(src + i2 + H);
+                    float4 v, v2;
+                    v.x = pq_f<FM>(a.x, b.x);
+                    v.y = pq_f<FM>(a.y, b.y);
+                    v.z = pq_f<FM>(a.z, b.z);
+                    v.w = pq_f<FM>(a.w, b.w);
+                    *reinterpret_cast<float4 *>(dst + i) = v;
+                    v2.x = pq_f<FM>(a2.x, b2.x);
+                    v2.y = pq_f<FM>(a2.y, b2.y);
+                    v2.z = pq_f<FM>(a2.z, b2.z);
+                    v2.w = pq_f<FM>(a2.w, b2.w);
+                    *reinterpret_cast<float4 *>(dst + i2) = v2;
+                    if (dmp) {
+                        *reinterpret_cast<float4 *>(dmp + i) = v;
+                        *reinterpret_cast<float4 *>(dmp + i2) = v2;
+                    }
+                }
+            } else
 #pragma unroll 1
             for (uint32_t i = 4 * tid; i < H; i += 4 * nthr) {
                 const float4 a = ch0 ? chan_load4(p, fc, i) : *reinterpret_cast<const float4 *>(src + i);
@@ -1405,7 +1441,7 @@ __global__ void fmag_kernel(const float *a, const float *b, float *out, int n)
 {
     load_log_table();
     if (FM == PQ_F_FIXED)
-        for (int i = threadIdx.x; i < 4097; i += blockDim.x) pq_phitab[i] = PHI_TAB_C[i];
+        for (int i = threadIdx.x; i < 4097; i += blockDim.x) pq_corrtab[i] = CORR_TAB_C[i];
     __syncthreads();
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) out[i] = pq_f<FM>(a[i], b[i]);
 }
@@ -1503,19 +1539,28 @@ static size_t dec_smem_bytes(uint32_t S)
 // Q8.8 phi table and the fixed-point rate-1 thresholds, computed
 // on the host (double-precision libm, rounded to nearest) and uploaded once
 // per device.  oracle/sc_oracle.c builds the same table the same way.
-static void fixed_tables(short *phi, float *tau)
+static void fixed_tables(float *corr, float *tau)
 {
-    phi[0] = 32767;
-    for (int k = 1; k <= 4096; k++) {
-        const long r = lrint(-log(tanh((double)k / 512.0)) * 256.0);
-        phi[k] = (short)(r > 32767 ? 32767 : r);
+    int C[4097];
+    for (int k = 0; k <= 4096; k++) {
+        C[k] = (int)lrint(log1p(exp(-(double)k / 256.0)) * 256.0);
+        corr[k] = (float)C[k];
     }
-    auto f = [&](int a, int b) {
-        const int s = std::min((int)phi[std::min(a, 4096)] + (int)phi[std::min(b, 4096)], 32767);
-        return std::min(std::min(a, b), (int)phi[std::min(s, 4096)]);
-    };
+    // L(a) = min over b >= a of |f(a, b)| = max(0, a + min_d (C[2a + d] - C[d]))
+    // (d = b - a; both indices clamp at 4096, so d <= 4096 covers every b)
+    std::vector<int> L(32768);
+    for (int a = 0; a < 32768; a++) {
+        int best = INT_MAX;
+        if (2 * a >= 4096) {
+            best = C[4096] - C[0];
+        } else {
+            for (int d = 0; d <= 4096; d++) best = std::min(best, C[std::min(2 * a + d, 4096)] - C[d]);
+        }
+        L[a] = std::max(0, a + best);
+    }
+    for (int a = 32766; a >= 0; a--) L[a] = std::min(L[a], L[a + 1]);  // suffix min: non-decreasing
     auto chain = [&](int t, int k) {
-        for (int i = 0; i < k; i++) t = f(t, t);
+        for (int i = 0; i < k; i++) t = L[t];
         return t;
     };
     for (int k = 0; k < 26; k++) {
@@ -1539,10 +1584,10 @@ static int ensure_fixed_tables()
     CUDA_TRY(cudaGetDevice(&dev));
     static bool done[64] = {false};
     if (dev < 64 && done[dev]) return 0;
-    short phi[4097];
+    static float corr[4097];
     float tau[26];
-    fixed_tables(phi, tau);
-    CUDA_TRY(cudaMemcpyToSymbol(PHI_TAB_C, phi, sizeof phi));
+    fixed_tables(corr, tau);
+    CUDA_TRY(cudaMemcpyToSymbol(CORR_TAB_C, corr, sizeof corr));
     CUDA_TRY(cudaMemcpyToSymbol(RATE1_TAU_FIX, tau, sizeof tau));
     if (dev < 64) done[dev] = true;
     return 0;

@@ -75,6 +75,10 @@ def phi(x):
 def _require_cuda(device=None):
     if torch is None or not torch.cuda.is_available():
         raise _lib.PolarScError("a CUDA device is required (no CPU fallback)")
+    if isinstance(device, torch.device):
+        if device.type != "cuda":
+            raise ValueError(f"device must be a CUDA device, got {device}")
+        device = device.index
     dev = torch.device("cuda", torch.cuda.current_device() if device is None else int(device))
     return dev
 

@@ -188,3 +188,41 @@ def test_de_oracle_acceptance6():
             _, leaf = O.sc_decode_naive(np.ones(8, np.uint8), llr, np.zeros(8, np.uint8))
             pe += prob * np.where(leaf < 0, 1.0, np.where(leaf == 0, 0.5, 0.0))
         assert np.max(np.abs(pe - de[f"pe_{p}"])) < 0.01
+
+
+def test_fixed_batch_driver_matches_single_frame():
+    """orc_sc_decode_batch(precision=16) = the fixed-point decoder on the
+    quantised LLRs, frame by frame, whatever the thread count."""
+    rng = np.random.default_rng(9)
+    n, F = 9, 6
+    N = 1 << n
+    mask = (rng.random(N) < 0.4).astype(np.uint8)
+    llr = rng.normal(0.7, 2.0, (F, N)).astype(np.float32)
+    fz = rng.integers(0, 2, (F, N)).astype(np.uint8)
+    ref = np.array([O.sc_decode_fixed(mask, O.quantize_q88(llr[f]), fz[f])[0] for f in range(F)])
+    for t in (1, 3):
+        assert np.array_equal(O.sc_decode_batch(mask, llr, fz, precision=16, threads=t), ref)
+
+
+def test_fixed_f_is_table_boxplus_within_2_lsb():
+    """The fixed-point f (read back through an n = 1 stage dump) is the exact
+    boxplus to within 2 LSB (three roundings of at most 1/2 LSB each), sign =
+    product of signs, |f| <= min(|a|, |b|); and the table is the spec'd form."""
+    corr = O.corr_table_q88()
+    k = np.arange(4097)
+    assert np.array_equal(corr, np.rint(256 * np.log1p(np.exp(-k / 256.0))).astype(np.int16))
+    rng = np.random.default_rng(31)
+    mask = np.array([0, 0], np.uint8)
+    for _ in range(3000):
+        a, b = (int(v) for v in rng.integers(-4000, 4001, 2))
+        _, _, st = O.sc_decode_fixed(mask, np.array([a, b], np.int16), np.zeros(2, np.uint8), dump=True)
+        f = int(st[1, 0])
+        assert abs(f) <= min(abs(a), abs(b))
+        if a and b and f:
+            assert (f < 0) == ((a < 0) != (b < 0))
+        if a == 0 or b == 0:
+            assert f == 0
+            continue
+        x, y = abs(a) / 256.0, abs(b) / 256.0
+        exact = min(x, y) + np.log1p(np.exp(-(x + y))) - np.log1p(np.exp(-abs(x - y)))
+        assert abs(abs(f) - 256 * exact) <= 2.0
