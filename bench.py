@@ -130,7 +130,7 @@ def oracle_precision(fmode):
     """The CPU decoder timed beside an f mode: the Q8.8 fixed-point port for
     --fmode fixed (the paper's Table-1 technique), else the
     f64 exact SC port."""
-    return (16, "Q8.8 fixed-point SC (phi table)") if fmode == "fixed" else (64, "f64 exact SC")
+    return (16, "Q8.8 fixed-point SC (table boxplus)") if fmode == "fixed" else (64, "f64 exact SC")
 
 
 def cpu_baseline(code, llr, u, sample_s, threads=1, precision=64):
@@ -147,7 +147,7 @@ def cpu_baseline(code, llr, u, sample_s, threads=1, precision=64):
         O.sc_decode_batch(code.frozen_mask, llr[idx], u[idx], precision=precision, threads=threads)
         done += k
         el = time.perf_counter() - t0
-        if el >= sample_s or done >= 4 * F:
+        if el >= sample_s or done >= 64 * F:
             break
     return done * N / el / 1e6, done, el
 
@@ -183,8 +183,8 @@ def roofline_entry(code, frames, log2S, t_kernel_s, peaks, band_share=None, fmod
 
 def with_traffic(roof, args):
     """dram read+write bytes per launch from the committed ncu --set full capture
-    of the same config/f mode (profiles/r01/ncu_full_<cfg>.json), if present."""
-    path = os.path.join(ROOT, "profiles", "r01", f"ncu_full_{args.config}.json")
+    of the same config/f mode (profiles/r01/ncu_full_<cfg>_<fmode>.json), if present."""
+    path = os.path.join(ROOT, "profiles", "r01", f"ncu_full_{args.config}_{args.fmode}.json")
     try:
         with open(path) as fh:
             cap = json.load(fh)
