@@ -278,6 +278,7 @@ def main():
     torch.cuda.synchronize()
     errors = int((uh != u_w).any(dim=1).sum().item())
     launches = dec.last_launches
+    ctas_per_frame = dec.last_ctas_per_frame
     log2S = dec_log2S(dec, F)
 
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
@@ -400,7 +401,7 @@ def main():
             "dtype": {"exact": "f32", "fast": "f32 (SFU transcendentals)", "fixed": "q8.8 (saturating int16 semantics)", "min-sum": "f32-minsum"}[args.fmode],
             "data": "synthetic: reference channel model, seeded (SURVEY 8(d)); reference-constructed frozen set",
             "config": {"workload": cfg.desc, "key": args.config, "frames_per_gpu": F, "N": N,
-                       "rate": cfg.rate, "f": args.fmode, "ssc": not args.no_ssc, "subtree_log2": log2S,
+                       "rate": cfg.rate, "f": args.fmode, "ssc": not args.no_ssc, "subtree_log2": log2S, "ctas_per_frame": ctas_per_frame,
                        "parallelism": f"frames sharded over {world} GPU(s)", "l2": "256 MiB flush between steps"},
             "fer": round(int(stats[0]) / int(stats[1]), 4), "frames_total": int(stats[1]),
             "e2e": e2e, "gpu_launches": launches * args.steps,

@@ -48,8 +48,10 @@ extern "C" {
 #define PQ_F_FAST 2
 /* FIXED: SPEC.md's sc_decode_fixed -- the reference's
  * default decode path: saturating Q8.8 LLRs (raw = sat(rint(256
- * L)) of the fp32 channel LLR), f = sgn min(|a|, |b|, phi(sat(phi|a| +
- * phi|b|))) with the 4096-entry phi table, saturating g.  Integer-exact: the
+ * L)) of the fp32 channel LLR), f = the exact boxplus by lookup in a 4097-entry
+ * table uniform on [0, 16]: sgn a sgn b max(0, min(|a|,|b|) + C[|a|+|b|] -
+ * C[||a|-|b||]), C[k] = rint(256 ln(1 + e^(-k/256))) (oracle/sc_oracle.c says
+ * why not the literal double phi lookup), saturating g.  Integer-exact: the
  * GPU reproduces the C oracle's decisions and stage values bit for bit.     */
 #define PQ_F_FIXED 3
 
@@ -57,9 +59,12 @@ extern "C" {
 #define PQ_OPT_SSC 1          /* 1 (default): skip rate-0/rate-1/repetition sub-trees
                                  (decision-exact); 0: plain SC          */
 #define PQ_OPT_SUBTREE_LOG2 2 /* log2 of the shared-memory sub-tree width S; 0 = auto  */
-#define PQ_OPT_FMODE 3        /* PQ_F_EXACT / PQ_F_MINSUM                              */
+#define PQ_OPT_FMODE 3        /* PQ_F_EXACT / PQ_F_MINSUM / PQ_F_FAST / PQ_F_FIXED     */
 #define PQ_OPT_PROFILE 4      /* 1: record per-frame clock64 cycles per step class      */
 #define PQ_OPT_WARP_LOG2 5    /* log2 of the widest node decoded by one warp (5..8, default 8) */
+#define PQ_OPT_CLUSTER 6      /* CTAs per frame for the upper band (a thread-block cluster):
+                                 0 = auto (more when frames < SMs), or 1, 2, 4, 8; it only
+                                 applies when the block has an upper band and S >= 2048   */
 
 /* slots of the per-frame profile record (pq_decoder_read_profile) */
 #define PQ_PROF_SLOTS 16
@@ -132,6 +137,9 @@ size_t pq_decoder_workspace_bytes(const pq_decoder *h);
 
 /* Number of kernels the last decode call launched (for bench accounting). */
 int pq_decoder_last_launches(const pq_decoder *h);
+
+/* CTAs per frame (thread-block cluster size) of the last decode launch. */
+int pq_decoder_last_ctas_per_frame(const pq_decoder *h);
 
 int pq_decoder_destroy(pq_decoder *h);
 

@@ -342,6 +342,7 @@ struct DecParams {
     int fixed;                   // 1: quantise channel LLRs to Q8.8 raw codes on load
     unsigned long long *prof;    // [F][PQ_PROF_SLOTS] clock64 cycles per step class, or null
     uint32_t wmax;               // widest node the single-warp band takes (32..256)
+    uint32_t K;                  // CTAs per frame (a thread-block cluster; 1, 2, 4 or 8)
 };
 
 // step classes for the optional per-frame cycle profile (PQ_OPT_PROFILE)
@@ -858,6 +859,20 @@ __device__ __forceinline__ void combine_block(uint32_t *x, uint32_t lpos, uint32
     for (uint32_t w = threadIdx.x; w < nw; w += blockDim.x) x[b + w] ^= x[b + nw + w];
 }
 
+// cluster-sliced word ranges of the global partial sums (W >= S >= 2048 bits,
+// so every CTA of a cluster of <= 8 gets >= 8 words): words [b, b + nw) = 0,
+// and words [b, b + nw) ^= words [b + nw, b + 2 nw)
+__device__ __forceinline__ void zero_words_slice(uint32_t *x, uint32_t b, uint32_t nw, uint32_t rank, uint32_t K)
+{
+    const uint32_t q = nw / K, w0 = rank * q;
+    for (uint32_t w = w0 + threadIdx.x; w < w0 + q; w += blockDim.x) x[b + w] = 0;
+}
+__device__ __forceinline__ void combine_words_slice(uint32_t *x, uint32_t b, uint32_t nw, uint32_t rank, uint32_t K)
+{
+    const uint32_t q = nw / K, w0 = rank * q;
+    for (uint32_t w = w0 + threadIdx.x; w < w0 + q; w += blockDim.x) x[b + w] ^= x[b + nw + w];
+}
+
 __device__ __forceinline__ float block_min(float v, float *red)
 {
     uint32_t m = __float_as_uint(v);
@@ -1038,7 +1053,35 @@ __device__ __forceinline__ void warp_small(const float *src, bool chan, const De
     if (lane == 0) put_bits(xs, pos, W, bits);
 }
 
-template <int FM>
+// ---- thread-block clusters: K CTAs share one frame's upper band
+// (configs with fewer frames than SMs).  Every step on a node wider than S is
+// split over the cluster's CTAs by contiguous slices and bracketed by a
+// cluster barrier (release/acquire at cluster scope orders the global-memory
+// stage buffers and partial sums between the CTAs); nodes of width <= S --
+// the shared-memory and single-warp bands -- run on the leader CTA (rank 0)
+// alone while the others wait at the next cluster barrier.
+__device__ __forceinline__ void cluster_sync_all()
+{
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
+// minimum over the cluster of one float per CTA (after a block_min)
+__device__ __forceinline__ float cluster_min(float m, float *slot, uint32_t K)
+{
+    if (threadIdx.x == 0) *slot = m;
+    cluster_sync_all();
+    float r = m;
+    for (uint32_t q = 0; q < K; q++) {
+        uint32_t a = (uint32_t)__cvta_generic_to_shared(slot), ra;
+        asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(a), "r"(q));
+        float v;
+        asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(v) : "r"(ra) : "memory");
+        r = fminf(r, v);
+    }
+    return r;
+}
+
+template <int FM, bool CL>
 __global__ void __launch_bounds__(256, 2) sc_decode_kernel(DecParams p)
 {
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -1054,7 +1097,11 @@ __global__ void __launch_bounds__(256, 2) sc_decode_kernel(DecParams p)
     if (FM == PQ_F_FIXED)
         for (int i = threadIdx.x; i < 4097; i += blockDim.x) pq_corrtab[i] = CORR_TAB_C[i];
     __syncthreads();
-    const uint32_t frame = blockIdx.x;
+    const uint32_t K = CL ? p.K : 1u;  // CL = false: the single-CTA path compiles without slicing
+    const uint32_t rank = blockIdx.x & (K - 1);  // CTA rank in the frame's cluster
+    const bool lead = rank == 0;
+    const uint32_t frame = blockIdx.x / K;
+    __shared__ float cl_slot;
     FrameCtx fc;
     fc.llr = p.llr ? p.llr + (size_t)frame * N : nullptr;
     fc.y = p.ybits ? p.ybits + (size_t)frame * p.wpf : nullptr;
@@ -1108,6 +1155,14 @@ __global__ void __launch_bounds__(256, 2) sc_decode_kernel(DecParams p)
     auto xptr = [&](uint32_t W) -> uint32_t * { return W <= S ? sm.xs : fc.X; };
     auto xpos = [&](uint32_t W, uint32_t pos) -> uint32_t { return W <= S ? (pos & (S - 1)) : pos; };
 
+    // barrier before a step on data wider than S: the whole cluster when K > 1
+    auto wsync = [&](bool wide) {
+        if (K > 1 && wide) cluster_sync_all();
+        else __syncthreads();
+    };
+    // this CTA's slice [lo, hi) of a range of L elements (L / K a multiple of 32)
+    auto slice_lo = [&](uint32_t L) -> uint32_t { return rank * (L / K); };
+
     int d = 0;
     uint32_t j = 0;
     bool entering = true;
@@ -1116,7 +1171,7 @@ __global__ void __launch_bounds__(256, 2) sc_decode_kernel(DecParams p)
     unsigned long long pr_acc[PQ_PROF_SLOTS];
     unsigned long long pr_last = 0, pr_start = 0;
     int pr_cls = PR_SM_OTHER;
-    const bool prof = p.prof != nullptr && tid == 32 * lw;  // the lower-band warp's lane 0
+    const bool prof = p.prof != nullptr && lead && tid == 32 * lw;  // the lower-band warp's lane 0
     if (prof) {
         for (int q = 0; q < PQ_PROF_SLOTS; q++) pr_acc[q] = 0;
         pr_start = pr_last = clock64();
@@ -1133,12 +1188,17 @@ __global__ void __launch_bounds__(256, 2) sc_decode_kernel(DecParams p)
     for (;;) {
         const uint32_t W = N >> d;
         if (entering) {
+            if (!lead && W <= S) {  // the leader decodes it; wait at the next cluster barrier
+                entering = false;
+                continue;
+            }
             uint8_t t = ntype(d, j);
             if (p.plain && W > 1) t = NT_MIXED;
             if (t == NT_RATE0) {
                 PROF_MARK(W > S ? PR_UP_OTHER : PR_SM_OTHER);
-                __syncthreads();
-                zero_bits_block(xptr(W), xpos(W, j * W), W);
+                wsync(W > S);
+                if (W > S) zero_words_slice(fc.X, (j * W) >> 5, W >> 5, rank, K);
+                else zero_bits_block(xptr(W), xpos(W, j * W), W);
                 entering = false;
                 continue;
             }
@@ -1197,23 +1257,26 @@ __global__ void __launch_bounds__(256, 2) sc_decode_kernel(DecParams p)
             const float *src = d == 0 ? nullptr : stage_ptr(p, fc, sm, W);
             if (t == NT_RATE1 && !p.plain) {
                 PROF_MARK(PR_RATE1);
-                __syncthreads();
+                wsync(W > S);
+                const bool split = K > 1 && W > S;
+                const uint32_t lo = split ? slice_lo(W) : 0, hi = split ? lo + W / K : W;
                 float m = __int_as_float(0x7f800000);
-                for (uint32_t i = tid; i < W; i += nthr) {
+                for (uint32_t i = lo + tid; i < hi; i += nthr) {
                     const float v = d == 0 ? chan_load(p, fc, i) : src[i];
                     m = fminf(m, fabsf(v));
                 }
                 m = block_min(m, red);
+                if (split) m = cluster_min(m, &cl_slot, K);
                 int k = 0;
                 for (uint32_t w = W; w > 1; w >>= 1) k++;
                 if (rate1_guard<FM>(m, k)) {
                     uint32_t *xb = xptr(W);
                     const uint32_t base = xpos(W, j * W) >> 5;
-                    for (uint32_t i0 = 0; i0 < W; i0 += nthr) {
+                    for (uint32_t i0 = lo; i0 < hi; i0 += nthr) {
                         const uint32_t i = i0 + tid;
-                        const float v = i < W ? (d == 0 ? chan_load(p, fc, i) : src[i]) : 0.0f;
+                        const float v = i < hi ? (d == 0 ? chan_load(p, fc, i) : src[i]) : 0.0f;
                         const uint32_t bits = __ballot_sync(0xffffffffu, v < 0.0f);
-                        if ((tid & 31) == 0 && i < W) xb[base + (i >> 5)] = bits;
+                        if ((tid & 31) == 0 && i < hi) xb[base + (i >> 5)] = bits;
                     }
                     entering = false;
                     continue;
@@ -1224,9 +1287,10 @@ __global__ void __launch_bounds__(256, 2) sc_decode_kernel(DecParams p)
             const uint8_t tl = p.plain ? NT_MIXED : ntype(d + 1, 2 * j);
             PROF_MARK(W > S ? PR_UP_F : PR_SM_F);
             if (prof) pr_acc[PR_NODES_BLOCK]++;
-            __syncthreads();
+            wsync(W > S);
             if (tl == NT_RATE0) {
-                zero_bits_block(xptr(H), xpos(H, 2 * j * H), H);
+                if (H > S) zero_words_slice(fc.X, (2 * j * H) >> 5, H >> 5, rank, K);
+                else if (lead) zero_bits_block(xptr(H), xpos(H, 2 * j * H), H);
                 d++;
                 j = 2 * j;
                 entering = false;
@@ -1237,10 +1301,16 @@ __global__ void __launch_bounds__(256, 2) sc_decode_kernel(DecParams p)
             // f-step, 4 consecutive elements per thread (H >= 256 here, so every
             // chunk is a whole float4)
             const bool ch0 = d == 0;
-            if (!ch0 && W > S && H % (8 * nthr) == 0) {
+            // a child wider than S is split over the cluster; one of width S
+            // lands in the leader's shared memory and is the leader's alone
+            const bool fsplit = K > 1 && H > S;
+            const uint32_t flo = fsplit ? slice_lo(H) : 0, fhi = fsplit ? flo + H / K : H;
+            if (!lead && !fsplit) {
+                // nothing for this CTA
+            } else if (!ch0 && W > S && (fhi - flo) % (8 * nthr) == 0) {
                 // from HBM/L2: two chunks per thread in flight
 #pragma unroll 1
-                for (uint32_t i = 4 * tid; i < H; i += 8 * nthr) {
+                for (uint32_t i = flo + 4 * tid; i < fhi; i += 8 * nthr) {
                     const uint32_t i2 = i + 4 * nthr;
                     const float4 a = *reinterpret_cast<const float4 *>(src + i);
                     const float4 b = *reinterpret_cast<const float4 *>(src + i + H);
@@ -1264,7 +1334,7 @@ __global__ void __launch_bounds__(256, 2) sc_decode_kernel(DecParams p)
                 }
             } else
 #pragma unroll 1
-            for (uint32_t i = 4 * tid; i < H; i += 4 * nthr) {
+            for (uint32_t i = flo + 4 * tid; i < fhi; i += 4 * nthr) {
                 const float4 a = ch0 ? chan_load4(p, fc, i) : *reinterpret_cast<const float4 *>(src + i);
                 const float4 b = ch0 ? chan_load4(p, fc, i + H) : *reinterpret_cast<const float4 *>(src + i + H);
                 float4 v;
@@ -1283,7 +1353,8 @@ __global__ void __launch_bounds__(256, 2) sc_decode_kernel(DecParams p)
         if (W == S && S < N) {
             PROF_MARK(PR_UP_OTHER);
             __syncthreads();
-            for (uint32_t w = tid; w < S / 32; w += nthr) fc.X[(j * S) / 32 + w] = sm.xs[w];
+            if (lead)
+                for (uint32_t w = tid; w < S / 32; w += nthr) fc.X[(j * S) / 32 + w] = sm.xs[w];
         }
         if (d == 0) {
             if (S >= N) {
@@ -1302,6 +1373,7 @@ __global__ void __launch_bounds__(256, 2) sc_decode_kernel(DecParams p)
                 pr_acc[14] = eng_prof[2];
                 for (int q = 0; q < PQ_PROF_SLOTS; q++) p.prof[(size_t)frame * PQ_PROF_SLOTS + q] = pr_acc[q];
             }
+            if (K > 1) cluster_sync_all();  // no CTA exits while a peer may read its shared memory
             break;
         }
         if ((j & 1) == 0) {
@@ -1309,9 +1381,10 @@ __global__ void __launch_bounds__(256, 2) sc_decode_kernel(DecParams p)
             const uint32_t jr = j + 1;
             const uint8_t tr = p.plain ? NT_MIXED : ntype(d, jr);
             PROF_MARK(2 * W > S ? PR_UP_G : PR_SM_G);
-            __syncthreads();
+            wsync(2 * W > S);
             if (tr == NT_RATE0) {
-                zero_bits_block(xptr(W), xpos(W, jr * W), W);
+                if (W > S) zero_words_slice(fc.X, (jr * W) >> 5, W >> 5, rank, K);
+                else if (lead) zero_bits_block(xptr(W), xpos(W, jr * W), W);
                 j = jr;
                 continue;  // still exiting: the right child is decided
             }
@@ -1322,15 +1395,17 @@ __global__ void __launch_bounds__(256, 2) sc_decode_kernel(DecParams p)
             float *dst = stage_ptr(p, fc, sm, W);
             float *dmp = fc.dump ? fc.dump + (size_t)d * N + (size_t)jr * W : nullptr;
             const bool ch0 = d - 1 == 0;
+            const bool gsplit = K > 1 && W > S;
+            const uint32_t glo = gsplit ? slice_lo(W) : 0, ghi = gsplit ? glo + W / K : (lead ? W : 0);
             // g-step: W >= 256 here; 4 elements per thread, 4 chunks in flight
 #pragma unroll 1
-            for (uint32_t base = 0; base < W; base += 16 * nthr) {
+            for (uint32_t base = glo; base < ghi; base += 16 * nthr) {
                 float4 a[4], b[4];
                 uint32_t sb[4];
 #pragma unroll
                 for (int k = 0; k < 4; k++) {
                     const uint32_t i = base + 4 * (tid + k * nthr);
-                    if (i < W) {
+                    if (i < ghi) {
                         a[k] = ch0 ? chan_load4(p, fc, i) : *reinterpret_cast<const float4 *>(src + i);
                         b[k] = ch0 ? chan_load4(p, fc, i + W) : *reinterpret_cast<const float4 *>(src + i + W);
                         sb[k] = (xl[(lpos + i) >> 5] >> ((lpos + i) & 31)) & 15u;
@@ -1339,7 +1414,7 @@ __global__ void __launch_bounds__(256, 2) sc_decode_kernel(DecParams p)
 #pragma unroll
                 for (int k = 0; k < 4; k++) {
                     const uint32_t i = base + 4 * (tid + k * nthr);
-                    if (i < W) {
+                    if (i < ghi) {
                         float4 v;
                         v.x = pq_gt<FM>(a[k].x, b[k].x, sb[k] & 1u);
                         v.y = pq_gt<FM>(a[k].y, b[k].y, sb[k] & 2u);
@@ -1356,8 +1431,9 @@ __global__ void __launch_bounds__(256, 2) sc_decode_kernel(DecParams p)
         }
         // right child done -> parent's partial sums = (xl ^ xr, xr)
         PROF_MARK(2 * W > S ? PR_UP_OTHER : PR_SM_OTHER);
-        __syncthreads();
-        combine_block(xptr(2 * W), xpos(2 * W, (j - 1) * W), W);
+        wsync(2 * W > S);
+        if (2 * W > S) combine_words_slice(fc.X, ((j - 1) * W) >> 5, W >> 5, rank, K);
+        else combine_block(xptr(2 * W), xpos(2 * W, (j - 1) * W), W);
         d--;
         j >>= 1;
     }
@@ -1509,8 +1585,51 @@ struct pq_decoder {
     int last_launches;
     int profile;
     int warp_log2;
+    int cluster_opt;  // PQ_OPT_CLUSTER: 0 = auto, else CTAs per frame
+    int last_K;       // CTAs per frame of the last decode launch
     unsigned long long *d_prof;
 };
+
+// CTAs per frame: split the upper band of a frame over a thread-block cluster
+// when frames alone leave SMs idle (e.g. c5: 32 frames on 148 SMs -> 4 CTAs
+// per frame).  Only with an upper band and S >= 2048 (every cluster slice of a
+// wide node is then >= 512 elements / 16 words).
+static int choose_K(const pq_decoder *h, int frames, int log2S, bool dump)
+{
+    if (dump || ((uint32_t)1 << log2S) >= h->N || log2S < 11) return 1;
+    if (h->cluster_opt > 0) return h->cluster_opt;
+    int K = 1;
+    while (K < 8 && (size_t)frames * K * 2 <= (size_t)h->sm_count) K *= 2;
+    return K;
+}
+
+template <int FM>
+static int launch_dec(const DecParams &p, int frames, size_t smem, cudaStream_t st)
+{
+    if (p.K == 1) {
+        CUDA_TRY(cudaFuncSetAttribute(sc_decode_kernel<FM, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)smem));
+        sc_decode_kernel<FM, false><<<frames, 256, smem, st>>>(p);
+        CUDA_TRY(cudaGetLastError());
+        return 0;
+    }
+    CUDA_TRY(cudaFuncSetAttribute(sc_decode_kernel<FM, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    cudaLaunchConfig_t cfg;
+    memset(&cfg, 0, sizeof cfg);
+    cfg.gridDim = dim3((unsigned)frames * p.K, 1, 1);
+    cfg.blockDim = dim3(256, 1, 1);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = p.K;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    CUDA_TRY(cudaLaunchKernelEx(&cfg, sc_decode_kernel<FM, true>, p));
+    return 0;
+}
 
 static int choose_log2S(const pq_decoder *h, int frames)
 {
@@ -1662,6 +1781,7 @@ int pq_decoder_destroy(pq_decoder *h)
 
 size_t pq_decoder_workspace_bytes(const pq_decoder *h) { return h ? h->ws_bytes : 0; }
 int pq_decoder_last_launches(const pq_decoder *h) { return h ? h->last_launches : 0; }
+int pq_decoder_last_ctas_per_frame(const pq_decoder *h) { return h ? h->last_K : 0; }
 
 int pq_decoder_set_option(pq_decoder *h, int key, int value)
 {
@@ -1680,6 +1800,11 @@ int pq_decoder_set_option(pq_decoder *h, int key, int value)
     case PQ_OPT_WARP_LOG2:
         if (value < 5 || value > 8) return set_err(-1, "warp band log2 width must be in 5..8");
         h->warp_log2 = value;
+        return 0;
+    case PQ_OPT_CLUSTER:
+        if (value != 0 && value != 1 && value != 2 && value != 4 && value != 8)
+            return set_err(-1, "cluster size must be 0 (auto), 1, 2, 4 or 8");
+        h->cluster_opt = value;
         return 0;
     case PQ_OPT_PROFILE:
         if (value && !h->d_prof) {
@@ -1711,6 +1836,7 @@ int pq_decoder_get_option(const pq_decoder *h, int key)
     case PQ_OPT_FMODE: return h->fmode;
     case PQ_OPT_PROFILE: return h->profile;
     case PQ_OPT_WARP_LOG2: return h->warp_log2;
+    case PQ_OPT_CLUSTER: return h->cluster_opt;
     default: return set_err(-1, "unknown option %d", key);
     }
 }
@@ -1805,25 +1931,15 @@ static int decode_impl(pq_decoder *h, const float *llr, const uint32_t *ybits, f
         if (rc) return rc;
         p.mag = fminf(fmaxf(rintf(mag * 256.0f), -32767.0f), 32767.0f);
     }
+    p.K = (uint32_t)choose_K(h, frames, p.log2S, dump != nullptr);
+    h->last_K = (int)p.K;
     const size_t smem = dec_smem_bytes(p.S);
-    if (h->fmode == PQ_F_FIXED) {
-        CUDA_TRY(cudaFuncSetAttribute(sc_decode_kernel<PQ_F_FIXED>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      (int)smem));
-        sc_decode_kernel<PQ_F_FIXED><<<frames, 256, smem, st>>>(p);
-    } else if (h->fmode == PQ_F_MINSUM) {
-        CUDA_TRY(cudaFuncSetAttribute(sc_decode_kernel<PQ_F_MINSUM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      (int)smem));
-        sc_decode_kernel<PQ_F_MINSUM><<<frames, 256, smem, st>>>(p);
-    } else if (h->fmode == PQ_F_FAST) {
-        CUDA_TRY(cudaFuncSetAttribute(sc_decode_kernel<PQ_F_FAST>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      (int)smem));
-        sc_decode_kernel<PQ_F_FAST><<<frames, 256, smem, st>>>(p);
-    } else {
-        CUDA_TRY(cudaFuncSetAttribute(sc_decode_kernel<PQ_F_EXACT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      (int)smem));
-        sc_decode_kernel<PQ_F_EXACT><<<frames, 256, smem, st>>>(p);
-    }
-    CUDA_TRY(cudaGetLastError());
+    int lrc;
+    if (h->fmode == PQ_F_FIXED) lrc = launch_dec<PQ_F_FIXED>(p, frames, smem, st);
+    else if (h->fmode == PQ_F_MINSUM) lrc = launch_dec<PQ_F_MINSUM>(p, frames, smem, st);
+    else if (h->fmode == PQ_F_FAST) lrc = launch_dec<PQ_F_FAST>(p, frames, smem, st);
+    else lrc = launch_dec<PQ_F_EXACT>(p, frames, smem, st);
+    if (lrc) return lrc;
     launches++;
     const size_t nwords = (size_t)frames * h->wpf;
     if (x_hat) {

@@ -137,6 +137,11 @@ class ScDecoder:
         _lib.check(_lib.load().pq_decoder_set_option(self._h, key, int(value)), "pq_decoder_set_option")
 
     @property
+    def last_ctas_per_frame(self) -> int:
+        """Thread-block cluster size (CTAs per frame) of the last decode."""
+        return int(_lib.load().pq_decoder_last_ctas_per_frame(self._h))
+
+    @property
     def workspace_bytes(self) -> int:
         return int(_lib.load().pq_decoder_workspace_bytes(self._h))
 

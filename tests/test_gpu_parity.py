@@ -517,3 +517,56 @@ def test_run_trials_counts_match_oracle(cuda, rep):
     assert row.trials == T and row.n == code.n
     assert row.fer_measured == expect / T
     assert row.throughput_mbps > 0
+
+
+# --------------------------------------------------------------------------
+# thread-block clusters: K CTAs per frame share the upper band
+
+def cluster_code(n, rng):
+    """Left quarter frozen (a wide rate-0 node), next quarter random, right
+    half information (a rate-1 node of width N/2 > S): exercises the
+    cluster-sliced rate-0 zeroing, the cluster-wide rate-1 minimum and the
+    sliced f/g/combine steps."""
+    N = 1 << n
+    mask = np.zeros(N, np.uint8)
+    mask[: N // 4] = 1
+    mask[N // 4: N // 2] = (rng.random(N // 4) < 0.5).astype(np.uint8)
+    return K.PolarCode(n=n, frozen_mask=mask, channel=C.BiAwgn(1.0), target_fer=0.1)
+
+
+@pytest.mark.parametrize("ncl", [2, 4, 8])
+@pytest.mark.parametrize("fmode", ["exact", "fixed"])
+def test_cluster_upper_band_bit_exact(cuda, ncl, fmode):
+    from paper_1204_5882_b200 import _lib
+    rng = np.random.default_rng(500 + ncl)
+    n, F = 15, 3
+    N = 1 << n
+    for code in (cluster_code(n, rng), random_code(n, 0.4, rng)):
+        # strong LLRs on frame 0 (rate-1 guard passes), weak ones elsewhere
+        llr = rng.normal(1.0, 2.0, (F, N)).astype(np.float32)
+        llr[0] = rng.normal(25.0, 2.0, N).astype(np.float32) * np.where(rng.random(N) < 0.2, -1, 1)
+        fz = rng.integers(0, 2, (F, N)).astype(np.uint8)
+        if fmode == "fixed":
+            ref = fixed_oracle_batch(code, O.quantize_q88(llr), fz)
+        else:
+            ref, _ = oracle_batch(code, llr, fz, 32)
+        dec = ScDecoder(code, max_frames=F, f_mode=fmode, subtree_log2=11)
+        dec.set_option(_lib.PQ_OPT_CLUSTER, ncl)
+        u, x = dec.decode(to_dev(llr, cuda), words_dev(fz, cuda), want_x=True)
+        assert np.array_equal(from_words(u, N), ref)
+        assert np.array_equal(from_words(x, N), transform_rows(from_words(u, N)))
+
+
+def test_cluster_auto_c5_shape_matches_single_cta(cuda):
+    """Auto cluster size on a few-frames N = 2^20 batch equals K = 1, bit for bit."""
+    from paper_1204_5882_b200 import _lib
+    if "c4" not in K.available_configs():
+        pytest.skip("c4 not built")
+    cfg, code, x, u_true, llr = config_batch("c4", 4)
+    outs = []
+    for ncl in (0, 1):
+        dec = ScDecoder(code, max_frames=4, f_mode="fixed")
+        dec.set_option(_lib.PQ_OPT_CLUSTER, ncl)
+        u, _ = dec.decode(to_dev(llr, cuda), words_dev(u_true, cuda))
+        outs.append(u.cpu().numpy())
+    assert np.array_equal(outs[0], outs[1])
