@@ -892,153 +892,185 @@ __device__ __forceinline__ float block_min(float v, float *red)
 // One warp decodes the sub-tree rooted at (d0, j0), width 32 <= W0 <= 256,
 // inside the shared-memory sub-tree: node values in the shared stage buffers
 // (width W at st_end - 2W), partial sums in xs (bit position (jW) mod S).
-// Nodes of width 32 go to the register decoder dec32; wider ones take
-// warp-synchronous f/g steps (<= 4 elements per lane, independent f's in
-// flight).  Everything else (types, R0/R1/REP shortcuts, partial-sum XORs)
-// mirrors the block walk, with __syncwarp instead of __syncthreads.
+// The walk is unrolled at compile time over the widths (walk_node<W> calls
+// walk_node<W/2> for both children): no loop-carried (d, j) state, every
+// per-lane element count is a constant, and the plain-SC/dump path is a
+// separate instantiation, so the SSC path carries no dump checks.  Nodes of
+// width 32 go to the register decoder dec32; wider ones take warp-synchronous
+// f/g steps (<= 4 elements per lane, independent f's in flight).
+struct WalkCtx {
+    float *st_end;
+    uint32_t *xs;
+    const uint8_t *ty;
+    float *dump;
+    uint32_t N;
+    int dS;
+    uint32_t jS;
+};
+
+// absolute (depth, index) of the node at S-local heap index lh (dump only)
+__device__ __forceinline__ NodePos walk_pos(const WalkCtx &c, uint32_t lh)
+{
+    const int e = ilog2(lh);
+    NodePos np;
+    np.dump = c.dump;
+    np.N = c.N;
+    np.d = c.dS + e;
+    np.j = (c.jS << e) + (lh - (1u << e));
+    return np;
+}
+
+template <int FM, bool PLAIN>
+__device__ __forceinline__ void walk_leaf32(const WalkCtx &c, uint32_t lh, uint32_t pos)
+{
+    const int lane = threadIdx.x & 31;
+    const float v = (c.st_end - 64)[lane];
+    const TypeBits T = load_typebits(c.ty, lh, 32, PLAIN);
+    NodePos np;
+    if (PLAIN) {
+        np = walk_pos(c, lh);
+    } else {
+        np.dump = nullptr;
+        np.N = c.N;
+        np.d = 0;
+        np.j = 0;
+    }
+    const uint32_t bits = dec32<FM>(v, T, PLAIN, np);
+    if (lane == 0) c.xs[pos >> 5] = bits;
+    __syncwarp();
+}
+
+template <int FM, bool PLAIN, int W>
+__device__ __forceinline__ void walk_node(const WalkCtx &c, uint32_t lh, uint32_t pos)
+{
+    constexpr uint32_t V = W / 32, H = W / 2, Vh = V / 2;
+    const unsigned FULL = 0xffffffffu;
+    const int lane = threadIdx.x & 31;
+    const float *nd = c.st_end - 2 * W;
+    uint32_t *xw = c.xs + (pos >> 5);  // this node's partial-sum words (V of them)
+    if (!PLAIN) {
+        const uint8_t t = c.ty[lh];
+        if (t == NT_RATE0) {
+            if (lane < (int)V) xw[lane] = 0;
+            __syncwarp();
+            return;
+        }
+        if (t == NT_RATE1) {
+            uint32_t m = 0x7f800000u;
+#pragma unroll
+            for (uint32_t q = 0; q < V; q++) m = min(m, __float_as_uint(nd[32 * q + lane]) & 0x7fffffffu);
+            m = __reduce_min_sync(FULL, m);
+            if (rate1_guard<FM>(__uint_as_float(m), ilog2(W))) {
+#pragma unroll
+                for (uint32_t q = 0; q < V; q++) {
+                    const uint32_t bits = __ballot_sync(FULL, nd[32 * q + lane] < 0.0f);
+                    if (lane == 0) xw[q] = bits;
+                }
+                __syncwarp();
+                return;
+            }
+        }
+        if (t == NT_REP) {
+            // SC's g-chain with zero partial sums, in SC's pairing order
+            float sm8[V];
+#pragma unroll
+            for (uint32_t q = 0; q < V; q++) sm8[q] = nd[32 * q + lane];
+#pragma unroll
+            for (uint32_t hv = V / 2; hv >= 1; hv >>= 1)
+#pragma unroll
+                for (uint32_t q = 0; q < hv; q++) sm8[q] = qadd<FM>(sm8[q + hv], sm8[q]);
+            float s0 = sm8[0];
+#pragma unroll
+            for (int hh = 16; hh >= 1; hh >>= 1) s0 = qadd<FM>(__shfl_down_sync(FULL, s0, hh), s0);
+            const uint32_t bits = __shfl_sync(FULL, s0, 0) < 0.0f ? FULL : 0u;
+            if (lane < (int)V) xw[lane] = bits;
+            __syncwarp();
+            return;
+        }
+    }
+    float *ch = c.st_end - W;  // stage buffer of both children
+    // ---- left child: f-step unless it is rate-0
+    if (!PLAIN && c.ty[2 * lh] == NT_RATE0) {
+        if (lane < (int)Vh) xw[lane] = 0;
+        __syncwarp();
+    } else {
+        float a[Vh], b[Vh];
+#pragma unroll
+        for (uint32_t q = 0; q < Vh; q++) {
+            a[q] = nd[32 * q + lane];
+            b[q] = nd[32 * q + lane + H];
+        }
+#pragma unroll
+        for (uint32_t q = 0; q < Vh; q++) {
+            const float v = pq_f<FM>(a[q], b[q]);
+            ch[32 * q + lane] = v;
+            if (PLAIN && c.dump) {
+                const NodePos np = walk_pos(c, 2 * lh);
+                c.dump[(size_t)np.d * c.N + (size_t)np.j * H + 32 * q + lane] = v;
+            }
+        }
+        __syncwarp();
+        if constexpr (H == 32) walk_leaf32<FM, PLAIN>(c, 2 * lh, pos);
+        else walk_node<FM, PLAIN, H>(c, 2 * lh, pos);
+    }
+    // ---- right child: g-step with the left child's partial sums
+    if (!PLAIN && c.ty[2 * lh + 1] == NT_RATE0) {
+        if (lane < (int)Vh) xw[Vh + lane] = 0;
+        __syncwarp();
+    } else {
+        float a[Vh], b[Vh];
+        uint32_t sw[Vh];
+#pragma unroll
+        for (uint32_t q = 0; q < Vh; q++) {
+            a[q] = nd[32 * q + lane];
+            b[q] = nd[32 * q + lane + H];
+            sw[q] = xw[q];
+        }
+#pragma unroll
+        for (uint32_t q = 0; q < Vh; q++) {
+            const float v = pq_gt<FM>(a[q], b[q], (sw[q] >> lane) & 1u);
+            ch[32 * q + lane] = v;
+            if (PLAIN && c.dump) {
+                const NodePos np = walk_pos(c, 2 * lh + 1);
+                c.dump[(size_t)np.d * c.N + (size_t)np.j * H + 32 * q + lane] = v;
+            }
+        }
+        __syncwarp();
+        if constexpr (H == 32) walk_leaf32<FM, PLAIN>(c, 2 * lh + 1, pos + H);
+        else walk_node<FM, PLAIN, H>(c, 2 * lh + 1, pos + H);
+    }
+    // ---- partial sums of this node: (xl ^ xr, xr)
+    if (lane < (int)Vh) xw[lane] ^= xw[Vh + lane];
+    __syncwarp();
+}
+
+template <int FM, bool PLAIN>
+__device__ __forceinline__ void walk_root(const WalkCtx &c, uint32_t W, uint32_t lh, uint32_t pos)
+{
+    if (W == 256) walk_node<FM, PLAIN, 256>(c, lh, pos);
+    else if (W == 128) walk_node<FM, PLAIN, 128>(c, lh, pos);
+    else if (W == 64) walk_node<FM, PLAIN, 64>(c, lh, pos);
+    else walk_leaf32<FM, PLAIN>(c, lh, pos);
+}
+
 template <int FM>
 __device__ __noinline__ void warp_walk(float *st_end, uint32_t *xs, const uint8_t *ty, float *dump, uint32_t N,
                                        uint32_t S, int dS, uint32_t jS, int plain_i, int d0, uint32_t j0)
 {
-    const unsigned FULL = 0xffffffffu;
-    const int lane = threadIdx.x & 31;
-    const bool plain = plain_i != 0;
-    int d = d0;
-    uint32_t j = j0;
-    bool entering = true;
-    for (;;) {
-        const uint32_t W = N >> d;
-        float *nd = st_end - 2 * W;
-        const int e = d - dS;
-        const uint32_t lh = (1u << e) + (j & ((1u << e) - 1u));
-        const uint32_t pos = (j * W) & (S - 1);
-        if (entering) {
-            const uint8_t t = plain ? NT_MIXED : ty[lh];
-            if (t == NT_RATE0) {
-                for (uint32_t w = lane; w < W / 32; w += 32) xs[(pos >> 5) + w] = 0;
-                __syncwarp();
-                entering = false;
-                continue;
-            }
-            if (W == 32) {
-                const float v = nd[lane];
-                const TypeBits T = load_typebits(ty, lh, 32, plain);
-                NodePos np;
-                np.dump = dump;
-                np.N = N;
-                np.d = d;
-                np.j = j;
-                const uint32_t bits = dec32<FM>(v, T, plain, np);
-                if (lane == 0) xs[pos >> 5] = bits;
-                __syncwarp();
-                entering = false;
-                continue;
-            }
-            const uint32_t V = W / 32;  // 2, 4 or 8 values per lane
-            if (t == NT_RATE1) {
-                uint32_t m = 0x7f800000u;
-                for (uint32_t q = 0; q < V; q++) m = min(m, __float_as_uint(nd[32 * q + lane]) & 0x7fffffffu);
-                m = __reduce_min_sync(FULL, m);
-                if (rate1_guard<FM>(__uint_as_float(m), ilog2(W))) {
-                    for (uint32_t q = 0; q < V; q++) {
-                        const uint32_t bits = __ballot_sync(FULL, nd[32 * q + lane] < 0.0f);
-                        if (lane == 0) xs[(pos >> 5) + q] = bits;
-                    }
-                    __syncwarp();
-                    entering = false;
-                    continue;
-                }
-            }
-            if (t == NT_REP) {
-                // SC's g-chain with zero partial sums, in SC's pairing order
-                float sm8[8];
-#pragma unroll
-                for (int q = 0; q < 8; q++) sm8[q] = q < (int)V ? nd[32 * q + lane] : 0.0f;
-                for (uint32_t hv = V / 2; hv >= 1; hv >>= 1)
-#pragma unroll
-                    for (int q = 0; q < 4; q++)
-                        if (q < (int)hv) sm8[q] = qadd<FM>(sm8[q + hv], sm8[q]);
-                float s0 = sm8[0];
-                for (int hh = 16; hh >= 1; hh >>= 1) {
-                    const float other = __shfl_down_sync(FULL, s0, hh);
-                    s0 = qadd<FM>(other, s0);
-                }
-                const uint32_t bits = __shfl_sync(FULL, s0, 0) < 0.0f ? FULL : 0u;
-                for (uint32_t w = lane; w < V; w += 32) xs[(pos >> 5) + w] = bits;
-                __syncwarp();
-                entering = false;
-                continue;
-            }
-            // mixed: f-step into the left child unless it is rate-0
-            const uint32_t H = W / 2, Vh = V / 2;
-            const uint8_t tl = plain ? NT_MIXED : ty[2 * lh];
-            if (tl == NT_RATE0) {
-                for (uint32_t w = lane; w < Vh; w += 32) xs[(pos >> 5) + w] = 0;
-                __syncwarp();
-                d++;
-                j = 2 * j;
-                entering = false;
-                continue;
-            }
-            float *ch = st_end - W;
-            float a[4], b[4];
-#pragma unroll
-            for (int q = 0; q < 4; q++)
-                if (q < (int)Vh) {
-                    a[q] = nd[32 * q + lane];
-                    b[q] = nd[32 * q + lane + H];
-                }
-#pragma unroll
-            for (int q = 0; q < 4; q++)
-                if (q < (int)Vh) {
-                    const float v = pq_f<FM>(a[q], b[q]);
-                    ch[32 * q + lane] = v;
-                    if (dump) dump[(size_t)(d + 1) * N + (size_t)(2 * j) * H + 32 * q + lane] = v;
-                }
-            __syncwarp();
-            d++;
-            j = 2 * j;
-            continue;
-        }
-        // ---- node (d, j) decided
-        if (d == d0) return;
-        if ((j & 1u) == 0) {
-            const uint8_t tr = plain ? NT_MIXED : ty[lh + 1];
-            const uint32_t posr = ((j + 1) * W) & (S - 1);
-            if (tr == NT_RATE0) {
-                for (uint32_t w = lane; w < W / 32; w += 32) xs[(posr >> 5) + w] = 0;
-                __syncwarp();
-                j++;
-                continue;
-            }
-            const float *par = st_end - 4 * W;
-            const uint32_t V = W / 32;
-            float a[4], b[4];
-            uint32_t sw[4];
-#pragma unroll
-            for (int q = 0; q < 4; q++)
-                if (q < (int)V) {
-                    a[q] = par[32 * q + lane];
-                    b[q] = par[32 * q + lane + W];
-                    sw[q] = xs[(pos >> 5) + q];
-                }
-#pragma unroll
-            for (int q = 0; q < 4; q++)
-                if (q < (int)V) {
-                    const float v = pq_gt<FM>(a[q], b[q], (sw[q] >> lane) & 1u);
-                    nd[32 * q + lane] = v;
-                    if (dump) dump[(size_t)d * N + (size_t)(j + 1) * W + 32 * q + lane] = v;
-                }
-            __syncwarp();
-            j++;
-            entering = true;
-            continue;
-        }
-        for (uint32_t w = lane; w < W / 32; w += 32) xs[((pos - W) >> 5) + w] ^= xs[(pos >> 5) + w];
-        __syncwarp();
-        d--;
-        j >>= 1;
-    }
+    WalkCtx c;
+    c.st_end = st_end;
+    c.xs = xs;
+    c.ty = ty;
+    c.dump = dump;
+    c.N = N;
+    c.dS = dS;
+    c.jS = jS;
+    const uint32_t W = N >> d0;
+    const int e = d0 - dS;
+    const uint32_t lh = (1u << e) + (j0 & ((1u << e) - 1u));
+    const uint32_t pos = (j0 * W) & (S - 1);
+    if (plain_i) walk_root<FM, true>(c, W, lh, pos);
+    else walk_root<FM, false>(c, W, lh, pos);
 }
 
 template <int FM>
