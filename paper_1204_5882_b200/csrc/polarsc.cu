@@ -503,8 +503,8 @@ __device__ __forceinline__ void dump_lanes(const NodePos &p, float v, int W)
 // ---- closed forms: the node's values are in registers of every lane; the
 // whole sub-tree is decided without shuffles or loops (uniform branches only)
 
-template <int FM>
-__device__ __forceinline__ uint32_t dec2(float a, float b, const TypeBits &T, int h, bool plain, const NodePos &np)
+template <int FM, bool plain>
+__device__ __forceinline__ uint32_t dec2(float a, float b, const TypeBits &T, int h, const NodePos &np)
 {
     const uint32_t t = plain ? NT_MIXED : tget(T, h);
     if (t == NT_RATE0) return 0u;
@@ -516,7 +516,7 @@ __device__ __forceinline__ uint32_t dec2(float a, float b, const TypeBits &T, in
     const uint32_t u0 = fa ? 0u : (l < 0.0f ? 1u : 0u);
     const float r = pq_gt<FM>(a, b, u0);
     const uint32_t u1 = fb ? 0u : (r < 0.0f ? 1u : 0u);
-    if (np.dump && (threadIdx.x & 31) == 0) {
+    if (plain && np.dump && (threadIdx.x & 31) == 0) {
         np.dump[(size_t)(np.d + 1) * np.N + 2 * np.j] = l;
         np.dump[(size_t)(np.d + 1) * np.N + 2 * np.j + 1] = r;
     }
@@ -525,9 +525,9 @@ __device__ __forceinline__ uint32_t dec2(float a, float b, const TypeBits &T, in
 
 // W = 4 node whose four values every lane holds: the whole sub-tree in
 // registers, no shuffles (uniform branches on the node types only).
-template <int FM>
+template <int FM, bool plain>
 __device__ __forceinline__ uint32_t dec4(float x0, float x1, float x2, float x3, const TypeBits &T, int h,
-                                         bool plain, const NodePos &np)
+                                         const NodePos &np)
 {
     const uint32_t t = plain ? NT_MIXED : tget(T, h);
     if (t == NT_RATE0) return 0u;
@@ -539,19 +539,19 @@ __device__ __forceinline__ uint32_t dec4(float x0, float x1, float x2, float x3,
     const bool lane0 = (threadIdx.x & 31) == 0;
     if (plain || tget(T, 2 * h) != NT_RATE0) {
         const float c0 = pq_f<FM>(x0, x2), c1 = pq_f<FM>(x1, x3);
-        if (np.dump && lane0) {
+        if (plain && np.dump && lane0) {
             np.dump[(size_t)(np.d + 1) * np.N + 4 * np.j] = c0;
             np.dump[(size_t)(np.d + 1) * np.N + 4 * np.j + 1] = c1;
         }
-        xl = dec2<FM>(c0, c1, T, 2 * h, plain, child_pos(np, 0));
+        xl = dec2<FM, plain>(c0, c1, T, 2 * h, child_pos(np, 0));
     }
     if (plain || tget(T, 2 * h + 1) != NT_RATE0) {
         const float c0 = pq_gt<FM>(x0, x2, xl & 1u), c1 = pq_gt<FM>(x1, x3, (xl >> 1) & 1u);
-        if (np.dump && lane0) {
+        if (plain && np.dump && lane0) {
             np.dump[(size_t)(np.d + 1) * np.N + 4 * np.j + 2] = c0;
             np.dump[(size_t)(np.d + 1) * np.N + 4 * np.j + 3] = c1;
         }
-        xr = dec2<FM>(c0, c1, T, 2 * h + 1, plain, child_pos(np, 1));
+        xr = dec2<FM, plain>(c0, c1, T, 2 * h + 1, child_pos(np, 1));
     }
     return ((xl ^ xr) & 3u) | (xr << 2);
 }
@@ -674,8 +674,8 @@ __device__ __forceinline__ bool w8_fast(float v, uint32_t pat, uint32_t &bits)
 
 // W = 8 node, lane i holds element i (lanes 0..7).  One copy (noinline):
 // lane-parallel f/g step, then the width-4 children in registers.
-template <int FM>
-__device__ __noinline__ uint32_t dec8(float v, const TypeBits T, int h, bool plain, const NodePos np)
+template <int FM, bool plain>
+__device__ __noinline__ uint32_t dec8(float v, const TypeBits T, int h, const NodePos np)
 {
     UB_BEGIN();
     const unsigned FULL = 0xffffffffu;
@@ -692,22 +692,22 @@ __device__ __noinline__ uint32_t dec8(float v, const TypeBits T, int h, bool pla
     uint32_t xl = 0, xr = 0;
     if (plain || tget(T, 2 * h) != NT_RATE0) {
         const float c = pq_f<FM>(v, b);
-        dump_lanes(child_pos(np, 0), c, 4);
-        xl = dec4<FM>(__shfl_sync(FULL, c, 0), __shfl_sync(FULL, c, 1), __shfl_sync(FULL, c, 2),
-                      __shfl_sync(FULL, c, 3), T, 2 * h, plain, child_pos(np, 0));
+        if (plain) dump_lanes(child_pos(np, 0), c, 4);
+        xl = dec4<FM, plain>(__shfl_sync(FULL, c, 0), __shfl_sync(FULL, c, 1), __shfl_sync(FULL, c, 2),
+                      __shfl_sync(FULL, c, 3), T, 2 * h, child_pos(np, 0));
     }
     if (plain || tget(T, 2 * h + 1) != NT_RATE0) {
         const float c = pq_gt<FM>(v, b, (xl >> ((threadIdx.x & 31) & 3)) & 1u);
-        dump_lanes(child_pos(np, 1), c, 4);
-        xr = dec4<FM>(__shfl_sync(FULL, c, 0), __shfl_sync(FULL, c, 1), __shfl_sync(FULL, c, 2),
-                      __shfl_sync(FULL, c, 3), T, 2 * h + 1, plain, child_pos(np, 1));
+        if (plain) dump_lanes(child_pos(np, 1), c, 4);
+        xr = dec4<FM, plain>(__shfl_sync(FULL, c, 0), __shfl_sync(FULL, c, 1), __shfl_sync(FULL, c, 2),
+                      __shfl_sync(FULL, c, 3), T, 2 * h + 1, child_pos(np, 1));
     }
     UB_END(0);
     return (xl ^ xr) | (xr << 4);
 }
 
-template <int FM>
-__device__ __forceinline__ uint32_t dec16(float v, const TypeBits &T, int h, bool plain, const NodePos &np)
+template <int FM, bool plain>
+__device__ __forceinline__ uint32_t dec16(float v, const TypeBits &T, int h, const NodePos &np)
 {
     const int lane = threadIdx.x & 31;
     uint32_t bits;
@@ -716,29 +716,29 @@ __device__ __forceinline__ uint32_t dec16(float v, const TypeBits &T, int h, boo
     uint32_t xl = 0, xr = 0;
     if (plain || tget(T, 2 * h) != NT_RATE0) {
         const float c = pq_f<FM>(v, b);
-        dump_lanes(child_pos(np, 0), c, 8);
-        xl = dec8<FM>(c, T, 2 * h, plain, child_pos(np, 0));
+        if (plain) dump_lanes(child_pos(np, 0), c, 8);
+        xl = dec8<FM, plain>(c, T, 2 * h, child_pos(np, 0));
     }
     if (plain || tget(T, 2 * h + 1) != NT_RATE0) {
         const float c = pq_gt<FM>(v, b, (xl >> (lane & 7)) & 1u);
-        dump_lanes(child_pos(np, 1), c, 8);
-        xr = dec8<FM>(c, T, 2 * h + 1, plain, child_pos(np, 1));
+        if (plain) dump_lanes(child_pos(np, 1), c, 8);
+        xr = dec8<FM, plain>(c, T, 2 * h + 1, child_pos(np, 1));
     }
     return (xl ^ xr) | (xr << 8);
 }
 
-template <int FM>
-__device__ __forceinline__ uint32_t dec32_body(float v, const TypeBits T, bool plain, const NodePos np);
-template <int FM>
-__device__ __noinline__ uint32_t dec32(float v, const TypeBits T, bool plain, const NodePos np)
+template <int FM, bool plain>
+__device__ __forceinline__ uint32_t dec32_body(float v, const TypeBits T, const NodePos np);
+template <int FM, bool plain>
+__device__ __noinline__ uint32_t dec32(float v, const TypeBits T, const NodePos np)
 {
     UB_BEGIN();
-    const uint32_t r = dec32_body<FM>(v, T, plain, np);
+    const uint32_t r = dec32_body<FM, plain>(v, T, np);
     UB_END(1);
     return r;
 }
-template <int FM>
-__device__ __forceinline__ uint32_t dec32_body(float v, const TypeBits T, bool plain, const NodePos np)
+template <int FM, bool plain>
+__device__ __forceinline__ uint32_t dec32_body(float v, const TypeBits T, const NodePos np)
 {
     const int lane = threadIdx.x & 31;
     uint32_t bits;
@@ -747,13 +747,13 @@ __device__ __forceinline__ uint32_t dec32_body(float v, const TypeBits T, bool p
     uint32_t xl = 0, xr = 0;
     if (plain || tget(T, 2) != NT_RATE0) {
         const float c = pq_f<FM>(v, b);
-        dump_lanes(child_pos(np, 0), c, 16);
-        xl = dec16<FM>(c, T, 2, plain, child_pos(np, 0));
+        if (plain) dump_lanes(child_pos(np, 0), c, 16);
+        xl = dec16<FM, plain>(c, T, 2, child_pos(np, 0));
     }
     if (plain || tget(T, 3) != NT_RATE0) {
         const float c = pq_gt<FM>(v, b, (xl >> (lane & 15)) & 1u);
-        dump_lanes(child_pos(np, 1), c, 16);
-        xr = dec16<FM>(c, T, 3, plain, child_pos(np, 1));
+        if (plain) dump_lanes(child_pos(np, 1), c, 16);
+        xr = dec16<FM, plain>(c, T, 3, child_pos(np, 1));
     }
     return (xl ^ xr) | (xr << 16);
 }
@@ -778,6 +778,21 @@ __device__ __forceinline__ TypeBits load_typebits(const uint8_t *ty, uint32_t ro
     return T;
 }
 
+template <int FM, bool plain>
+__device__ __forceinline__ uint32_t engine32_dispatch(float A, int W0, const TypeBits &T, const NodePos &np)
+{
+    if (W0 == 32) return dec32<FM, plain>(A, T, np);
+    if (W0 == 16) return dec16<FM, plain>(A, T, 2, np);
+    if (W0 == 8) return dec8<FM, plain>(A, T, 4, np);
+    float x[4];
+#pragma unroll
+    for (int i = 0; i < 4; i++) x[i] = __shfl_sync(0xffffffffu, A, i);
+    if (W0 == 4) return dec4<FM, plain>(x[0], x[1], x[2], x[3], T, 8, np);
+    if (W0 == 2) return dec2<FM, plain>(x[0], x[1], T, 16, np);
+    // W0 == 1: a single leaf
+    return ((T.leaf & 1u) || !(x[0] < 0.0f)) ? 0u : 1u;
+}
+
 // Decode the node at S-local heap index `root` of width W0 <= 32 whose
 // values are held one per lane in A (lane l = element l).  Returns its bits.
 template <int FM>
@@ -790,17 +805,8 @@ __device__ __forceinline__ uint32_t engine32_body(float A, uint32_t root, int W0
     np.N = c.N;
     np.d = c.dS + el;
     np.j = (c.jS << el) + (root - (1u << el));
-    const bool plain = c.plain != 0;
-    if (W0 == 32) return dec32<FM>(A, T, plain, np);
-    if (W0 == 16) return dec16<FM>(A, T, 2, plain, np);
-    if (W0 == 8) return dec8<FM>(A, T, 4, plain, np);
-    float x[4];
-#pragma unroll
-    for (int i = 0; i < 4; i++) x[i] = __shfl_sync(0xffffffffu, A, i);
-    if (W0 == 4) return dec4<FM>(x[0], x[1], x[2], x[3], T, 8, plain, np);
-    if (W0 == 2) return dec2<FM>(x[0], x[1], T, 16, plain, np);
-    // W0 == 1: a single leaf
-    return ((T.leaf & 1u) || !(x[0] < 0.0f)) ? 0u : 1u;
+    if (c.plain) return engine32_dispatch<FM, true>(A, W0, T, np);
+    return engine32_dispatch<FM, false>(A, W0, T, np);
 }
 
 template <int FM>
@@ -935,7 +941,7 @@ __device__ __forceinline__ void walk_leaf32(const WalkCtx &c, uint32_t lh, uint3
         np.d = 0;
         np.j = 0;
     }
-    const uint32_t bits = dec32<FM>(v, T, PLAIN, np);
+    const uint32_t bits = dec32<FM, PLAIN>(v, T, np);
     if (lane == 0) c.xs[pos >> 5] = bits;
     __syncwarp();
 }
