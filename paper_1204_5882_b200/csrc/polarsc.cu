@@ -447,8 +447,8 @@ __device__ unsigned long long g_ub_time[16], g_ub_count[16];
 #define UB_END(slot)                                                   \
     do {                                                               \
         if ((threadIdx.x & 31) == 0) {                                 \
-            g_ub_time[slot] += clock64() - ub_t0_;                     \
-            g_ub_count[slot] += 1;                                     \
+            atomicAdd(&g_ub_time[slot], (unsigned long long)(clock64() - ub_t0_)); \
+            atomicAdd(&g_ub_count[slot], 1ull);                        \
         }                                                              \
     } while (0)
 #else
@@ -578,16 +578,11 @@ __device__ __forceinline__ bool lanes_special(float v, int W, uint32_t t, uint32
         }
     }
     if (t == NT_REP) {
-        // all values to every lane, then SC's g-chain sum in its pairing order
-        float x[32];
-#pragma unroll
-        for (int i = 0; i < 32; i++) x[i] = i < W ? __shfl_sync(FULL, v, i) : 0.0f;
-#pragma unroll
-        for (int hh = 16; hh >= 1; hh >>= 1)
-            if (hh < W)
-#pragma unroll
-                for (int i = 0; i < hh; i++) x[i] = qadd<FM>(x[i + hh], x[i]);
-        bits = x[0] < 0.0f ? lowmask(W) : 0u;
+        // SC's g-chain sum in its pairing order, x[i] <- x[i + hh] + x[i] for
+        // hh = W/2 .. 1: a shuffle-down tree (lane i < hh reads lane i + hh < W)
+        float x = v;
+        for (int hh = W >> 1; hh >= 1; hh >>= 1) x = qadd<FM>(__shfl_down_sync(FULL, x, hh), x);
+        bits = __shfl_sync(FULL, x, 0) < 0.0f ? lowmask(W) : 0u;
         return true;
     }
     return false;
@@ -681,11 +676,11 @@ __device__ __noinline__ uint32_t dec8(float v, const TypeBits T, int h, const No
     const unsigned FULL = 0xffffffffu;
     uint32_t bits;
     if (!plain && tget(T, h) == NT_MIXED && w8_fast<FM>(v, (T.leaf >> (8 * (h - 4))) & 0xffu, bits)) {
-        UB_END(0);
+        UB_END(4);
         return bits;
     }
     if (!plain && lanes_special<FM>(v, 8, tget(T, h), bits)) {
-        UB_END(0);
+        UB_END(5);
         return bits;
     }
     const float b = __shfl_down_sync(FULL, v, 4);
@@ -709,9 +704,13 @@ __device__ __noinline__ uint32_t dec8(float v, const TypeBits T, int h, const No
 template <int FM, bool plain>
 __device__ __forceinline__ uint32_t dec16(float v, const TypeBits &T, int h, const NodePos &np)
 {
+    UB_BEGIN();
     const int lane = threadIdx.x & 31;
     uint32_t bits;
-    if (!plain && lanes_special<FM>(v, 16, tget(T, h), bits)) return bits;
+    if (!plain && lanes_special<FM>(v, 16, tget(T, h), bits)) {
+        UB_END(6);
+        return bits;
+    }
     const float b = __shfl_down_sync(0xffffffffu, v, 8);
     uint32_t xl = 0, xr = 0;
     if (plain || tget(T, 2 * h) != NT_RATE0) {
@@ -724,6 +723,7 @@ __device__ __forceinline__ uint32_t dec16(float v, const TypeBits &T, int h, con
         if (plain) dump_lanes(child_pos(np, 1), c, 8);
         xr = dec8<FM, plain>(c, T, 2 * h + 1, child_pos(np, 1));
     }
+    UB_END(3);
     return (xl ^ xr) | (xr << 8);
 }
 
@@ -1075,8 +1075,10 @@ __device__ __noinline__ void warp_walk(float *st_end, uint32_t *xs, const uint8_
     const int e = d0 - dS;
     const uint32_t lh = (1u << e) + (j0 & ((1u << e) - 1u));
     const uint32_t pos = (j0 * W) & (S - 1);
+    UB_BEGIN();
     if (plain_i) walk_root<FM, true>(c, W, lh, pos);
     else walk_root<FM, false>(c, W, lh, pos);
+    UB_END(2);
 }
 
 template <int FM>
@@ -1820,6 +1822,22 @@ int pq_decoder_destroy(pq_decoder *h)
 size_t pq_decoder_workspace_bytes(const pq_decoder *h) { return h ? h->ws_bytes : 0; }
 int pq_decoder_last_launches(const pq_decoder *h) { return h ? h->last_launches : 0; }
 int pq_decoder_last_ctas_per_frame(const pq_decoder *h) { return h ? h->last_K : 0; }
+
+#ifdef PQ_UBENCH_TIMING
+// instrumented builds only (tools/ub_profile.py): per-slot cycles and calls
+int pq_debug_ub(unsigned long long *out, int reset)
+{
+    CUDA_TRY(cudaDeviceSynchronize());
+    CUDA_TRY(cudaMemcpyFromSymbol(out, g_ub_time, sizeof(unsigned long long) * 16));
+    CUDA_TRY(cudaMemcpyFromSymbol(out + 16, g_ub_count, sizeof(unsigned long long) * 16));
+    if (reset) {
+        unsigned long long z[16] = {0};
+        CUDA_TRY(cudaMemcpyToSymbol(g_ub_time, z, sizeof z));
+        CUDA_TRY(cudaMemcpyToSymbol(g_ub_count, z, sizeof z));
+    }
+    return 0;
+}
+#endif
 
 int pq_decoder_set_option(pq_decoder *h, int key, int value)
 {
