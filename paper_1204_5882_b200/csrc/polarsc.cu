@@ -1093,6 +1093,179 @@ __device__ __forceinline__ void warp_small(const float *src, bool chan, const De
     if (lane == 0) put_bits(xs, pos, W, bits);
 }
 
+// ---- upper band through a TMA ring.  A frame's upper band is one CTA (or
+// cluster) streaming its stage vectors through HBM/L2; with register loads
+// the bytes in flight per CTA -- and so the per-frame bandwidth -- are capped
+// by registers (measured: latency-bound, ~17 GB/s per frame).  Instead one
+// thread issues 1-D bulk copies (cp.async.bulk, the TMA engine) of C-element
+// chunks of both operands (plus the bit words the step needs) into a ring of
+// D stages in the shared-memory stage area (idle during upper steps), with
+// an mbarrier per stage; the CTA consumes chunk c while chunks c+1..c+D-1
+// are in flight.  Only steps whose output stays in global memory use it (the
+// ring occupies the whole stage area); the f/g-steps into a width-S child
+// keep the register path.
+
+__device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count)
+{
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes)
+{
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity)
+{
+    asm volatile(
+        "{\n\t.reg .pred P1;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+        "@!P1 bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar)
+{
+    asm volatile("cp.async.bulk.shared::cta.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+
+__device__ __forceinline__ void fence_proxy_async()
+{
+    asm volatile("fence.proxy.async;" ::: "memory");
+}
+
+// one upper step's operands: A/B element vectors (fp32 stage or channel
+// LLRs), or the channel's received bits; optional coset words; optional
+// left-child partial sums (g-steps).  Offsets are element indices.
+struct UpSrc {
+    const float *a, *b;          // stage or fp32 channel halves (null: BSC bits)
+    const uint32_t *ya, *yb;     // BSC received-bit halves (or null)
+    const uint32_t *ca, *cb;     // coset words of the halves (or null)
+    const uint32_t *xl;          // g-step: left-child partial sums (bit e of the range), or null
+    bool chan;                   // operands are channel LLRs (quantise in fixed mode, coset flips)
+};
+
+struct Ring {
+    uint64_t *bar;   // D mbarriers
+    float *base;     // ring start in shared memory
+    uint32_t C;      // elements per chunk (multiple of 256)
+    uint32_t D;      // stages
+    uint32_t sbytes; // bytes per stage
+};
+
+// stage layout: [A: C floats][B: C floats][ya][yb][ca][cb][xl] (C/32 words each)
+__device__ __forceinline__ void ring_issue(const Ring &r, const UpSrc &u, uint32_t e0, uint32_t s)
+{
+    unsigned char *st = reinterpret_cast<unsigned char *>(r.base) + (size_t)s * r.sbytes;
+    const uint32_t C = r.C, wb = C / 8;  // bytes of C bits
+    uint32_t bytes = 0;
+    if (u.a) bytes += 8 * C;
+    if (u.ya) bytes += 2 * wb;
+    if (u.ca) bytes += 2 * wb;
+    if (u.xl) bytes += wb;
+    mbar_expect_tx(&r.bar[s], bytes);
+    if (u.a) {
+        bulk_g2s(st, u.a + e0, 4 * C, &r.bar[s]);
+        bulk_g2s(st + 4 * C, u.b + e0, 4 * C, &r.bar[s]);
+    }
+    if (u.ya) {
+        bulk_g2s(st + 8 * C, u.ya + e0 / 32, wb, &r.bar[s]);
+        bulk_g2s(st + 8 * C + wb, u.yb + e0 / 32, wb, &r.bar[s]);
+    }
+    if (u.ca) {
+        bulk_g2s(st + 8 * C + 2 * wb, u.ca + e0 / 32, wb, &r.bar[s]);
+        bulk_g2s(st + 8 * C + 3 * wb, u.cb + e0 / 32, wb, &r.bar[s]);
+    }
+    if (u.xl) bulk_g2s(st + 8 * C + 4 * wb, u.xl + e0 / 32, wb, &r.bar[s]);
+}
+
+// four consecutive operands (k % 4 == 0) of one half from a landed stage
+template <int FM>
+__device__ __forceinline__ float4 ring_val4(const DecParams &p, const UpSrc &u, const unsigned char *st,
+                                            uint32_t C, int half, uint32_t k)
+{
+    const uint32_t wb = C / 8;
+    const uint32_t *cw = reinterpret_cast<const uint32_t *>(st + 8 * C + (2 + half) * wb);
+    const uint32_t c4 = u.ca ? (cw[k >> 5] >> (k & 31)) & 15u : 0u;
+    float4 v;
+    if (u.ya) {
+        const uint32_t *yw = reinterpret_cast<const uint32_t *>(st + 8 * C + half * wb);
+        const uint32_t y4 = ((yw[k >> 5] >> (k & 31)) & 15u) ^ c4;
+        v.x = (y4 & 1u) ? -p.mag : p.mag;
+        v.y = (y4 & 2u) ? -p.mag : p.mag;
+        v.z = (y4 & 4u) ? -p.mag : p.mag;
+        v.w = (y4 & 8u) ? -p.mag : p.mag;
+        return v;
+    }
+    v = *reinterpret_cast<const float4 *>(st + (size_t)half * 4 * C + 4 * k);
+    if (u.chan) {
+        if (p.fixed) {  // channel LLRs -> Q8.8 codes on load, as chan_load4
+            v.x = fminf(fmaxf(rintf(v.x * 256.0f), -Q_MAX), Q_MAX);
+            v.y = fminf(fmaxf(rintf(v.y * 256.0f), -Q_MAX), Q_MAX);
+            v.z = fminf(fmaxf(rintf(v.z * 256.0f), -Q_MAX), Q_MAX);
+            v.w = fminf(fmaxf(rintf(v.w * 256.0f), -Q_MAX), Q_MAX);
+        }
+        v.x = __uint_as_float(__float_as_uint(v.x) ^ ((c4 & 1u) << 31));
+        v.y = __uint_as_float(__float_as_uint(v.y) ^ ((c4 & 2u) << 30));
+        v.z = __uint_as_float(__float_as_uint(v.z) ^ ((c4 & 4u) << 29));
+        v.w = __uint_as_float(__float_as_uint(v.w) ^ ((c4 & 8u) << 28));
+    }
+    return v;
+}
+
+// One upper step over output elements [lo, hi) of this CTA through the ring:
+// f-step (IS_G = false) or g-step with the left child's partial sums.
+// dst: the output stage vector (global, or shared memory for a width-S
+// child).  All threads call it; thread 0 issues the copies.  ph holds the
+// CTA-uniform parity bit of every stage's mbarrier.
+template <int FM, bool IS_G>
+__device__ __forceinline__ void ring_step(const DecParams &p, const Ring &r, const UpSrc &u, float *dst, uint32_t lo,
+                                          uint32_t hi, uint32_t &ph)
+{
+    const uint32_t C = r.C, D = r.D, tid = threadIdx.x, nthr = blockDim.x;
+    const uint32_t nch = (hi - lo) / C;
+    if (tid == 0)
+        for (uint32_t c = 0; c < nch && c < D; c++) ring_issue(r, u, lo + c * C, c);
+    uint32_t s = 0;
+    for (uint32_t c = 0; c < nch; c++) {
+        mbar_wait(&r.bar[s], (ph >> s) & 1u);
+        ph ^= 1u << s;
+        const unsigned char *st = reinterpret_cast<const unsigned char *>(r.base) + (size_t)s * r.sbytes;
+        const uint32_t e0 = lo + c * C;
+#pragma unroll 1
+        for (uint32_t k = 4 * tid; k < C; k += 4 * nthr) {
+            const float4 a = ring_val4<FM>(p, u, st, C, 0, k);
+            const float4 b = ring_val4<FM>(p, u, st, C, 1, k);
+            float4 v;
+            if (IS_G) {
+                const uint32_t *xw = reinterpret_cast<const uint32_t *>(st + 8 * C + 4 * (C / 8));
+                const uint32_t sb = (xw[k >> 5] >> (k & 31)) & 15u;
+                v.x = pq_gt<FM>(a.x, b.x, sb & 1u);
+                v.y = pq_gt<FM>(a.y, b.y, sb & 2u);
+                v.z = pq_gt<FM>(a.z, b.z, sb & 4u);
+                v.w = pq_gt<FM>(a.w, b.w, sb & 8u);
+            } else {
+                v.x = pq_f<FM>(a.x, b.x);
+                v.y = pq_f<FM>(a.y, b.y);
+                v.z = pq_f<FM>(a.z, b.z);
+                v.w = pq_f<FM>(a.w, b.w);
+            }
+            *reinterpret_cast<float4 *>(dst + e0 + k) = v;
+        }
+        __syncthreads();  // stage s fully consumed
+        if (tid == 0 && c + D < nch) ring_issue(r, u, lo + (c + D) * C, s);
+        s = s + 1 == D ? 0 : s + 1;
+    }
+}
+
 // ---- thread-block clusters: K CTAs share one frame's upper band
 // (configs with fewer frames than SMs).  Every step on a node wider than S is
 // split over the cluster's CTAs by contiguous slices and bracketed by a
@@ -1164,6 +1337,28 @@ __global__ void __launch_bounds__(256, 2) sc_decode_kernel(DecParams p)
     __syncthreads();
     const int lw = lw_sh;
     const uint32_t WMAX = S < p.wmax ? S : p.wmax;  // nodes this wide or narrower: one warp
+
+    // TMA ring for the upper band (S >= 2048 so that chunks are >= 256 elements;
+    // the stage dump keeps the register path)
+    __shared__ __align__(8) uint64_t ring_bar[8];
+    const bool use_ring = S >= 2048 && p.dump == nullptr;
+    uint32_t ring_ph = 0;
+    if (use_ring) {
+        if (tid == 0) {
+            for (int q = 0; q < 8; q++) mbar_init(&ring_bar[q], 1);
+            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        }
+        __syncthreads();
+    }
+    // two stages of S/4-element chunks over the stage area (A/B-measured on
+    // c3: chunk size matters -- S/8 was 8 % slower -- depth 2 vs 3 does not:
+    // with every frame streaming, the upper band then runs near HBM peak)
+    Ring ring;
+    ring.bar = ring_bar;
+    ring.C = S / 4;
+    ring.sbytes = 8 * ring.C + 5 * (ring.C / 8);
+    ring.D = 2;
+    ring.base = sm.st;
 
     __shared__ unsigned long long eng_prof[4];
     if (tid < 4) eng_prof[tid] = 0;
@@ -1327,6 +1522,9 @@ __global__ void __launch_bounds__(256, 2) sc_decode_kernel(DecParams p)
             const uint8_t tl = p.plain ? NT_MIXED : ntype(d + 1, 2 * j);
             PROF_MARK(W > S ? PR_UP_F : PR_SM_F);
             if (prof) pr_acc[PR_NODES_BLOCK]++;
+            // every writer orders its generic-proxy stores before the barrier that
+            // precedes the ring's bulk (async-proxy) reads of them
+            if (use_ring && H > S) fence_proxy_async();
             wsync(W > S);
             if (tl == NT_RATE0) {
                 if (H > S) zero_words_slice(fc.X, (2 * j * H) >> 5, H >> 5, rank, K);
@@ -1347,6 +1545,27 @@ __global__ void __launch_bounds__(256, 2) sc_decode_kernel(DecParams p)
             const uint32_t flo = fsplit ? slice_lo(H) : 0, fhi = fsplit ? flo + H / K : H;
             if (!lead && !fsplit) {
                 // nothing for this CTA
+            } else if (use_ring && H > S) {
+                UpSrc u;
+                memset(&u, 0, sizeof u);
+                if (ch0) {
+                    u.chan = true;
+                    if (fc.llr) {
+                        u.a = fc.llr;
+                        u.b = fc.llr + H;
+                    } else {
+                        u.ya = fc.y;
+                        u.yb = fc.y + H / 32;
+                    }
+                    if (fc.cw) {
+                        u.ca = fc.cw;
+                        u.cb = fc.cw + H / 32;
+                    }
+                } else {
+                    u.a = src;
+                    u.b = src + H;
+                }
+                ring_step<FM, false>(p, ring, u, dst, flo, fhi, ring_ph);
             } else if (!ch0 && W > S && (fhi - flo) % (8 * nthr) == 0) {
                 // from HBM/L2: two chunks per thread in flight
 #pragma unroll 1
@@ -1421,6 +1640,7 @@ __global__ void __launch_bounds__(256, 2) sc_decode_kernel(DecParams p)
             const uint32_t jr = j + 1;
             const uint8_t tr = p.plain ? NT_MIXED : ntype(d, jr);
             PROF_MARK(2 * W > S ? PR_UP_G : PR_SM_G);
+            if (use_ring && W > S) fence_proxy_async();
             wsync(2 * W > S);
             if (tr == NT_RATE0) {
                 if (W > S) zero_words_slice(fc.X, (jr * W) >> 5, W >> 5, rank, K);
@@ -1437,9 +1657,33 @@ __global__ void __launch_bounds__(256, 2) sc_decode_kernel(DecParams p)
             const bool ch0 = d - 1 == 0;
             const bool gsplit = K > 1 && W > S;
             const uint32_t glo = gsplit ? slice_lo(W) : 0, ghi = gsplit ? glo + W / K : (lead ? W : 0);
+            const bool gring = use_ring && W > S;
+            if (gring && ghi > glo) {
+                UpSrc u;
+                memset(&u, 0, sizeof u);
+                if (ch0) {
+                    u.chan = true;
+                    if (fc.llr) {
+                        u.a = fc.llr;
+                        u.b = fc.llr + W;
+                    } else {
+                        u.ya = fc.y;
+                        u.yb = fc.y + W / 32;
+                    }
+                    if (fc.cw) {
+                        u.ca = fc.cw;
+                        u.cb = fc.cw + W / 32;
+                    }
+                } else {
+                    u.a = src;
+                    u.b = src + W;
+                }
+                u.xl = fc.X + (j * W) / 32;  // the left child's bits (a width-S child's were copied out)
+                ring_step<FM, true>(p, ring, u, dst, glo, ghi, ring_ph);
+            }
             // g-step: W >= 256 here; 4 elements per thread, 4 chunks in flight
 #pragma unroll 1
-            for (uint32_t base = glo; base < ghi; base += 16 * nthr) {
+            for (uint32_t base = glo; base < (gring ? glo : ghi); base += 16 * nthr) {
                 float4 a[4], b[4];
                 uint32_t sb[4];
 #pragma unroll
