@@ -46,6 +46,8 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--fmode", default="fixed", choices=["exact", "fast", "fixed", "min-sum"])
     ap.add_argument("--no-ssc", action="store_true")
+    ap.add_argument("--threads", type=int, default=0, choices=[0, 128, 256], help="threads per CTA (0 = auto)")
+    ap.add_argument("--cluster", type=int, default=0, choices=[0, 1, 2, 4, 8], help="CTAs per frame (0 = auto)")
     ap.add_argument("--cpu-sample-s", type=float, default=10.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -266,6 +268,11 @@ def main():
     u_w = polar_transform_words(x_w, n)  # Alice: u = T(x); the decoder reads u at frozen positions
     llr_d = torch.from_numpy(llr).to(dev)
     dec = ScDecoder(code, max_frames=F, f_mode=args.fmode, ssc=not args.no_ssc)
+    from paper_1204_5882_b200 import _lib
+    if args.threads:
+        dec.set_option(_lib.PQ_OPT_THREADS, args.threads)
+    if args.cluster:
+        dec.set_option(_lib.PQ_OPT_CLUSTER, args.cluster)
     uh = dec.alloc_words(F)
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.int32, device=dev)  # 256 MiB > L2
     stream = torch.cuda.current_stream()
@@ -278,8 +285,8 @@ def main():
     torch.cuda.synchronize()
     errors = int((uh != u_w).any(dim=1).sum().item())
     launches = dec.last_launches
-    ctas_per_frame = dec.last_ctas_per_frame
-    log2S = dec_log2S(dec, F)
+    launch_cfg = dec.last_config
+    log2S = launch_cfg["subtree_log2"]
 
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     if world > 1:
@@ -401,7 +408,8 @@ def main():
             "dtype": {"exact": "f32", "fast": "f32 (SFU transcendentals)", "fixed": "q8.8 (saturating int16 semantics)", "min-sum": "f32-minsum"}[args.fmode],
             "data": "synthetic: reference channel model, seeded (SURVEY 8(d)); reference-constructed frozen set",
             "config": {"workload": cfg.desc, "key": args.config, "frames_per_gpu": F, "N": N,
-                       "rate": cfg.rate, "f": args.fmode, "ssc": not args.no_ssc, "subtree_log2": log2S, "ctas_per_frame": ctas_per_frame,
+                       "rate": cfg.rate, "f": args.fmode, "ssc": not args.no_ssc, "subtree_log2": log2S, "threads_per_cta": launch_cfg["threads_per_cta"],
+                       "ctas_per_frame": launch_cfg["ctas_per_frame"],
                        "parallelism": f"frames sharded over {world} GPU(s)", "l2": "256 MiB flush between steps"},
             "fer": round(int(stats[0]) / int(stats[1]), 4), "frames_total": int(stats[1]),
             "e2e": e2e, "gpu_launches": launches * args.steps,
@@ -413,19 +421,6 @@ def main():
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
-
-
-def dec_log2S(dec, F):
-    """Mirror of the library's automatic sub-tree size choice (for reporting)."""
-    import torch
-    sm = torch.cuda.get_device_properties(dec.device).multi_processor_count
-    per_sm = -(-F // sm)
-    best = 6
-    for k in range(6, 15):
-        S = 1 << k
-        if per_sm * (8 * S + (S // 32) * 4 + 2 * S) <= 200 * 1024:
-            best = k
-    return min(best, dec.n)
 
 
 if __name__ == "__main__":

@@ -65,6 +65,8 @@ extern "C" {
 #define PQ_OPT_CLUSTER 6      /* CTAs per frame for the upper band (a thread-block cluster):
                                  0 = auto (more when frames < SMs), or 1, 2, 4, 8; it only
                                  applies when the block has an upper band and S >= 2048   */
+#define PQ_OPT_THREADS 7      /* threads per CTA: 0 = auto (256 up to 2 frames per SM, else
+                                 128 so that 4 frames share an SM), or 128 / 256            */
 
 /* slots of the per-frame profile record (pq_decoder_read_profile) */
 #define PQ_PROF_SLOTS 16
@@ -140,6 +142,10 @@ int pq_decoder_last_launches(const pq_decoder *h);
 
 /* CTAs per frame (thread-block cluster size) of the last decode launch. */
 int pq_decoder_last_ctas_per_frame(const pq_decoder *h);
+
+/* Launch shape of the last decode: log2 of the shared-memory sub-tree width
+ * S, threads per CTA, CTAs per frame (any pointer may be NULL).            */
+int pq_decoder_last_config(const pq_decoder *h, int *log2S, int *threads_per_cta, int *ctas_per_frame);
 
 int pq_decoder_destroy(pq_decoder *h);
 

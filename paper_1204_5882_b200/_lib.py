@@ -23,6 +23,7 @@ PQ_OPT_FMODE = 3
 PQ_OPT_PROFILE = 4
 PQ_OPT_WARP_LOG2 = 5
 PQ_OPT_CLUSTER = 6
+PQ_OPT_THREADS = 7
 PQ_PROF_SLOTS = 16
 PROF_NAMES = ("upper_f", "upper_g", "upper_other", "smem_f", "smem_g", "smem_other", "warp_subtrees",
               "type_staging", "rate1_block", "total", "n_warp_subtrees", "n_block_nodes",
@@ -34,7 +35,7 @@ EXPORTS = (
     "pq_decoder_get_option", "pq_sc_decode_f32", "pq_sc_decode_f32_dump", "pq_sc_decode_bsc",
     "pq_polar_transform", "pq_decoder_workspace_bytes", "pq_decoder_last_launches",
     "pq_decoder_destroy", "pq_last_error", "pq_abi_version", "pq_decoder_read_profile",
-    "pq_debug_fmag", "pq_decoder_last_ctas_per_frame",
+    "pq_debug_fmag", "pq_decoder_last_ctas_per_frame", "pq_decoder_last_config",
 )
 
 _lib = None
@@ -67,6 +68,7 @@ def load():
     L.pq_decoder_workspace_bytes.restype = ctypes.c_size_t
     L.pq_decoder_last_launches.argtypes = [vp]
     L.pq_decoder_last_ctas_per_frame.argtypes = [vp]
+    L.pq_decoder_last_config.argtypes = [vp, vp, vp, vp]
     L.pq_decoder_destroy.argtypes = [vp]
     L.pq_decoder_read_profile.argtypes = [vp, vp, i]
     L.pq_debug_fmag.argtypes = [i, vp, vp, vp, i, vp]

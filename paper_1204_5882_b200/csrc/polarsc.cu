@@ -1332,7 +1332,7 @@ __global__ void __launch_bounds__(256, 2) sc_decode_kernel(DecParams p)
     if (tid == 0) {
         uint32_t ws;
         asm volatile("mov.u32 %0, %%warpid;" : "=r"(ws));
-        lw_sh = (int)((ws >> 3) & 3u);
+        lw_sh = (int)((ws / (uint32_t)(nthr >> 5)) & 3u);
     }
     __syncthreads();
     const int lw = lw_sh;
@@ -1870,7 +1870,9 @@ struct pq_decoder {
     int profile;
     int warp_log2;
     int cluster_opt;  // PQ_OPT_CLUSTER: 0 = auto, else CTAs per frame
+    int threads_opt;  // PQ_OPT_THREADS: 0 = auto, else 128 or 256 threads per CTA
     int last_K;       // CTAs per frame of the last decode launch
+    int last_log2S, last_threads;
     unsigned long long *d_prof;
 };
 
@@ -1888,12 +1890,12 @@ static int choose_K(const pq_decoder *h, int frames, int log2S, bool dump)
 }
 
 template <int FM>
-static int launch_dec(const DecParams &p, int frames, size_t smem, cudaStream_t st)
+static int launch_dec(const DecParams &p, int frames, int nthreads, size_t smem, cudaStream_t st)
 {
     if (p.K == 1) {
         CUDA_TRY(cudaFuncSetAttribute(sc_decode_kernel<FM, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       (int)smem));
-        sc_decode_kernel<FM, false><<<frames, 256, smem, st>>>(p);
+        sc_decode_kernel<FM, false><<<frames, nthreads, smem, st>>>(p);
         CUDA_TRY(cudaGetLastError());
         return 0;
     }
@@ -1901,7 +1903,7 @@ static int launch_dec(const DecParams &p, int frames, size_t smem, cudaStream_t 
     cudaLaunchConfig_t cfg;
     memset(&cfg, 0, sizeof cfg);
     cfg.gridDim = dim3((unsigned)frames * p.K, 1, 1);
-    cfg.blockDim = dim3(256, 1, 1);
+    cfg.blockDim = dim3(nthreads, 1, 1);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
     cudaLaunchAttribute at[1];
@@ -1915,19 +1917,32 @@ static int launch_dec(const DecParams &p, int frames, size_t smem, cudaStream_t 
     return 0;
 }
 
-static int choose_log2S(const pq_decoder *h, int frames)
+// threads per CTA: 256 when frames leave <= 2 per SM (latency: a frame's
+// block steps get 8 warps), else 128 (throughput: the 128-register kernel then
+// fits 4 CTAs -- 4 serial warps, one per SM sub-partition -- per SM)
+static int choose_threads(const pq_decoder *h, int frames)
+{
+    if (h->threads_opt) return h->threads_opt;
+    return frames > 2 * h->sm_count ? 128 : 256;
+}
+
+static int choose_log2S(const pq_decoder *h, int frames, int nthreads)
 {
     const int lo = h->n < 6 ? h->n : 6;  // warp sub-trees (W <= 64) must sit inside S
     if (h->log2S_opt > 0) {
         int k = h->log2S_opt < h->n ? h->log2S_opt : h->n;
         return k < lo ? lo : k;
     }
-    const int per_sm = (frames + h->sm_count - 1) / h->sm_count;
+    // resident CTAs per SM (the kernel's 128 registers per thread cap them)
+    const int cap = nthreads == 128 ? 4 : 2;
+    int per_sm = (frames + h->sm_count - 1) / h->sm_count;
+    if (per_sm > cap) per_sm = cap;
+    if (per_sm < 1) per_sm = 1;
     int best = 6;
     for (int k = 6; k <= 14; k++) {
         const size_t S = (size_t)1 << k;
-        const size_t bytes = 8 * S + (S / 32) * 4 + 2 * S;
-        if ((size_t)per_sm * bytes <= 200 * 1024) best = k;
+        const size_t bytes = 8 * S + (S / 32) * 4 + 2 * S + 18 * 1024;  // + static (table, barriers)
+        if ((size_t)per_sm * bytes <= 226 * 1024) best = k;
     }
     if (best > h->n) best = h->n;
     return best;
@@ -2067,6 +2082,15 @@ size_t pq_decoder_workspace_bytes(const pq_decoder *h) { return h ? h->ws_bytes 
 int pq_decoder_last_launches(const pq_decoder *h) { return h ? h->last_launches : 0; }
 int pq_decoder_last_ctas_per_frame(const pq_decoder *h) { return h ? h->last_K : 0; }
 
+int pq_decoder_last_config(const pq_decoder *h, int *log2S, int *threads_per_cta, int *ctas_per_frame)
+{
+    if (!h) return set_err(-1, "handle is NULL");
+    if (log2S) *log2S = h->last_log2S;
+    if (threads_per_cta) *threads_per_cta = h->last_threads;
+    if (ctas_per_frame) *ctas_per_frame = h->last_K;
+    return 0;
+}
+
 #ifdef PQ_UBENCH_TIMING
 // instrumented builds only (tools/ub_profile.py): per-slot cycles and calls
 int pq_debug_ub(unsigned long long *out, int reset)
@@ -2100,6 +2124,10 @@ int pq_decoder_set_option(pq_decoder *h, int key, int value)
     case PQ_OPT_WARP_LOG2:
         if (value < 5 || value > 8) return set_err(-1, "warp band log2 width must be in 5..8");
         h->warp_log2 = value;
+        return 0;
+    case PQ_OPT_THREADS:
+        if (value != 0 && value != 128 && value != 256) return set_err(-1, "threads must be 0 (auto), 128 or 256");
+        h->threads_opt = value;
         return 0;
     case PQ_OPT_CLUSTER:
         if (value != 0 && value != 1 && value != 2 && value != 4 && value != 8)
@@ -2137,6 +2165,7 @@ int pq_decoder_get_option(const pq_decoder *h, int key)
     case PQ_OPT_PROFILE: return h->profile;
     case PQ_OPT_WARP_LOG2: return h->warp_log2;
     case PQ_OPT_CLUSTER: return h->cluster_opt;
+    case PQ_OPT_THREADS: return h->threads_opt;
     default: return set_err(-1, "unknown option %d", key);
     }
 }
@@ -2209,7 +2238,8 @@ static int decode_impl(pq_decoder *h, const float *llr, const uint32_t *ybits, f
     DecParams p;
     memset(&p, 0, sizeof p);
     p.n = h->n;
-    p.log2S = choose_log2S(h, frames);
+    const int nthreads = choose_threads(h, frames);
+    p.log2S = choose_log2S(h, frames, nthreads);
     p.plain = (dump || !h->ssc) ? 1 : 0;
     p.frames = frames;
     p.N = h->N;
@@ -2233,12 +2263,14 @@ static int decode_impl(pq_decoder *h, const float *llr, const uint32_t *ybits, f
     }
     p.K = (uint32_t)choose_K(h, frames, p.log2S, dump != nullptr);
     h->last_K = (int)p.K;
+    h->last_log2S = p.log2S;
+    h->last_threads = nthreads;
     const size_t smem = dec_smem_bytes(p.S);
     int lrc;
-    if (h->fmode == PQ_F_FIXED) lrc = launch_dec<PQ_F_FIXED>(p, frames, smem, st);
-    else if (h->fmode == PQ_F_MINSUM) lrc = launch_dec<PQ_F_MINSUM>(p, frames, smem, st);
-    else if (h->fmode == PQ_F_FAST) lrc = launch_dec<PQ_F_FAST>(p, frames, smem, st);
-    else lrc = launch_dec<PQ_F_EXACT>(p, frames, smem, st);
+    if (h->fmode == PQ_F_FIXED) lrc = launch_dec<PQ_F_FIXED>(p, frames, nthreads, smem, st);
+    else if (h->fmode == PQ_F_MINSUM) lrc = launch_dec<PQ_F_MINSUM>(p, frames, nthreads, smem, st);
+    else if (h->fmode == PQ_F_FAST) lrc = launch_dec<PQ_F_FAST>(p, frames, nthreads, smem, st);
+    else lrc = launch_dec<PQ_F_EXACT>(p, frames, nthreads, smem, st);
     if (lrc) return lrc;
     launches++;
     const size_t nwords = (size_t)frames * h->wpf;

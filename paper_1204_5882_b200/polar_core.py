@@ -137,6 +137,15 @@ class ScDecoder:
         _lib.check(_lib.load().pq_decoder_set_option(self._h, key, int(value)), "pq_decoder_set_option")
 
     @property
+    def last_config(self) -> dict:
+        """Launch shape of the last decode: sub-tree width log2, threads per
+        CTA, CTAs per frame."""
+        vals = [ctypes.c_int(0) for _ in range(3)]
+        _lib.check(_lib.load().pq_decoder_last_config(self._h, *[ctypes.byref(v) for v in vals]),
+                   "pq_decoder_last_config")
+        return {"subtree_log2": vals[0].value, "threads_per_cta": vals[1].value, "ctas_per_frame": vals[2].value}
+
+    @property
     def last_ctas_per_frame(self) -> int:
         """Thread-block cluster size (CTAs per frame) of the last decode."""
         return int(_lib.load().pq_decoder_last_ctas_per_frame(self._h))
