@@ -48,6 +48,7 @@ def parse():
     ap.add_argument("--no-ssc", action="store_true")
     ap.add_argument("--threads", type=int, default=0, choices=[0, 128, 256], help="threads per CTA (0 = auto)")
     ap.add_argument("--cluster", type=int, default=0, choices=[0, 1, 2, 4, 8], help="CTAs per frame (0 = auto)")
+    ap.add_argument("--warp-log2", type=int, default=0, help="widest node of the single-warp band, log2 (0 = default)")
     ap.add_argument("--cpu-sample-s", type=float, default=10.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -273,6 +274,8 @@ def main():
         dec.set_option(_lib.PQ_OPT_THREADS, args.threads)
     if args.cluster:
         dec.set_option(_lib.PQ_OPT_CLUSTER, args.cluster)
+    if args.warp_log2:
+        dec.set_option(_lib.PQ_OPT_WARP_LOG2, args.warp_log2)
     uh = dec.alloc_words(F)
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.int32, device=dev)  # 256 MiB > L2
     stream = torch.cuda.current_stream()

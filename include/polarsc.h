@@ -61,7 +61,7 @@ extern "C" {
 #define PQ_OPT_SUBTREE_LOG2 2 /* log2 of the shared-memory sub-tree width S; 0 = auto  */
 #define PQ_OPT_FMODE 3        /* PQ_F_EXACT / PQ_F_MINSUM / PQ_F_FAST / PQ_F_FIXED     */
 #define PQ_OPT_PROFILE 4      /* 1: record per-frame clock64 cycles per step class      */
-#define PQ_OPT_WARP_LOG2 5    /* log2 of the widest node decoded by one warp (5..8, default 8) */
+#define PQ_OPT_WARP_LOG2 5    /* log2 of the widest node decoded by one warp (5..9, default 9) */
 #define PQ_OPT_CLUSTER 6      /* CTAs per frame for the upper band (a thread-block cluster):
                                  0 = auto (more when frames < SMs), or 1, 2, 4, 8; it only
                                  applies when the block has an upper band and S >= 2048   */

@@ -1053,7 +1053,8 @@ __device__ __forceinline__ void walk_node(const WalkCtx &c, uint32_t lh, uint32_
 template <int FM, bool PLAIN>
 __device__ __forceinline__ void walk_root(const WalkCtx &c, uint32_t W, uint32_t lh, uint32_t pos)
 {
-    if (W == 256) walk_node<FM, PLAIN, 256>(c, lh, pos);
+    if (W == 512) walk_node<FM, PLAIN, 512>(c, lh, pos);
+    else if (W == 256) walk_node<FM, PLAIN, 256>(c, lh, pos);
     else if (W == 128) walk_node<FM, PLAIN, 128>(c, lh, pos);
     else if (W == 64) walk_node<FM, PLAIN, 64>(c, lh, pos);
     else walk_leaf32<FM, PLAIN>(c, lh, pos);
@@ -2032,7 +2033,7 @@ int pq_decoder_create(pq_decoder **out, int n, int max_frames, int f_mode, int d
     h->device = device;
     h->ssc = 1;
     h->log2S_opt = 0;
-    h->warp_log2 = 8;
+    h->warp_log2 = 9;
     h->N = 1u << n;
     h->wpf = h->N >= 32 ? h->N / 32 : 1;
     cudaDeviceProp prop;
@@ -2122,7 +2123,7 @@ int pq_decoder_set_option(pq_decoder *h, int key, int value)
         h->fmode = value;
         return 0;
     case PQ_OPT_WARP_LOG2:
-        if (value < 5 || value > 8) return set_err(-1, "warp band log2 width must be in 5..8");
+        if (value < 5 || value > 9) return set_err(-1, "warp band log2 width must be in 5..9");
         h->warp_log2 = value;
         return 0;
     case PQ_OPT_THREADS:
