@@ -146,7 +146,7 @@ int main()
         uint8_t *tyh = (uint8_t *)malloc(2048);
         FILE *fp = fopen("tools/ubench/c1_types.bin", "rb");
         if (fp) {
-            fread(tyh, 1, 2048, fp);
+            if (fread(tyh, 1, 2048, fp) != 2048) return 1;
             fclose(fp);
             float *lh = (float *)malloc(4096);
             uint32_t seed = 1;
@@ -166,20 +166,8 @@ int main()
             cudaMemcpy(&c, cyc, 8, cudaMemcpyDeviceToHost);
             printf("c1 warp levels, MIN-SUM f: %lld cycles\n", c);
             for (int r = 0; r < 2; r++) k_c1_warp<PQ_F_EXACT><<<1, 32>>>(dty, dl, cyc, dout, 10);
-            {
-                int z = 0;
-                cudaMemcpyToSymbol(g_ub_ntrace, &z, sizeof z);
-                k_c1_warp<PQ_F_EXACT><<<1, 32>>>(dty, dl, cyc, dout, 1);
-                cudaDeviceSynchronize();
-                int nt;
-                cudaMemcpyFromSymbol(&nt, g_ub_ntrace, sizeof nt);
-                static long long tr[8192];
-                cudaMemcpyFromSymbol(tr, g_ub_trace, sizeof tr);
-                FILE *fo = fopen("gpurun_out/trace.txt", "w");
-                for (int q = 0; q < nt; q++)
-                    fprintf(fo, "%lld %lld %lld %lld\n", tr[4 * q] - tr[0], tr[4 * q + 1], tr[4 * q + 2], tr[4 * q + 3]);
-                fclose(fo);
-            }
+            k_c1_warp<PQ_F_EXACT><<<1, 32>>>(dty, dl, cyc, dout, 1);
+            cudaDeviceSynchronize();
             cudaMemcpy(&c, cyc, 8, cudaMemcpyDeviceToHost);
             printf("c1 warp levels (4 x W256 sub-trees): %lld cycles\n", c);
             unsigned long long tt[16], cc[16];

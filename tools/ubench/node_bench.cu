@@ -4,6 +4,18 @@
 #define FMX PQ_F_EXACT
 #endif
 
+template <int MODE, bool PL>
+__device__ __forceinline__ uint32_t node(float v, const TypeBits &T, const NodePos &np)
+{
+    if (MODE == 8) return dec8<FMX, PL>(v, T, 1, np);
+    if (MODE == 32) return dec32<FMX, PL>(v, T, np);
+    if (MODE == 16) return dec16<FMX, PL>(v, T, 1, np);
+    if (MODE == 4)
+        return dec4<FMX, PL>(__shfl_sync(0xffffffffu, v, 0), __shfl_sync(0xffffffffu, v, 1), __shfl_sync(0xffffffffu, v, 2),
+                             __shfl_sync(0xffffffffu, v, 3), T, 1, np);
+    return dec2<FMX, PL>(v, __shfl_sync(0xffffffffu, v, 1), T, 1, np);
+}
+
 template <int MODE>
 __global__ void k_node(const float *in, long long *cyc, uint32_t *out, int iters, uint32_t tb0, uint32_t tb1,
                        uint32_t leaf, int plain)
@@ -24,11 +36,8 @@ __global__ void k_node(const float *in, long long *cyc, uint32_t *out, int iters
     long long t0 = clock64();
     for (int i = 0; i < iters; i++) {
         uint32_t r;
-        if (MODE == 8) r = dec8<FMX>(v, T, 1, plain != 0, np);
-        else if (MODE == 32) r = dec32<FMX>(v, T, plain != 0, np);
-        else if (MODE == 16) r = dec16<FMX>(v, T, 1, plain != 0, np);
-        else if (MODE == 4) r = dec4<FMX>(__shfl_sync(0xffffffffu, v, 0), __shfl_sync(0xffffffffu, v, 1), __shfl_sync(0xffffffffu, v, 2), __shfl_sync(0xffffffffu, v, 3), T, 1, plain != 0, np);
-        else r = dec2<FMX>(v, __shfl_sync(0xffffffffu, v, 1), T, 1, plain != 0, np);
+        if (plain) r = node<MODE, true>(v, T, np);
+        else r = node<MODE, false>(v, T, np);
         acc += r;
         v = v + 1e-7f * (float)(r & 1u);  // carry a dependency into the next call
     }
