@@ -110,6 +110,13 @@ int pq_sc_decode_f32_dump(pq_decoder *h, const float *llr, const uint32_t *froze
                           uint32_t *u_hat, uint32_t *x_hat, float *dump, int frames,
                           void *stream);
 
+/* SPEC.md's sc_decode_fixed(code, llrs-fixed, frozen_values):
+ * channel LLRs given as saturating Q8.8 raw codes (int16, |raw| <= 32767,
+ * e.g. sat(rint(256 L))), [frames][N] frame-major.  Needs a PQ_F_FIXED
+ * decoder; otherwise as pq_sc_decode_f32 (half its input bytes).          */
+int pq_sc_decode_q88(pq_decoder *h, const int16_t *llr_q88, const uint32_t *frozen_u,
+                     uint32_t *u_hat, uint32_t *x_hat, int frames, void *stream);
+
 /* BSC front end fused into the decoder's level-0 reads: y_bits are Bob's
  * received bits packed like u_hat; the channel LLR (1-2y)*llr_mag is formed
  * on the fly (channel.py:142-147 with magnitude min(30, ln((1-p)/p))).

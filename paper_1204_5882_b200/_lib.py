@@ -35,7 +35,7 @@ EXPORTS = (
     "pq_decoder_get_option", "pq_sc_decode_f32", "pq_sc_decode_f32_dump", "pq_sc_decode_bsc",
     "pq_polar_transform", "pq_decoder_workspace_bytes", "pq_decoder_last_launches",
     "pq_decoder_destroy", "pq_last_error", "pq_abi_version", "pq_decoder_read_profile",
-    "pq_debug_fmag", "pq_decoder_last_ctas_per_frame", "pq_decoder_last_config",
+    "pq_debug_fmag", "pq_decoder_last_ctas_per_frame", "pq_decoder_last_config", "pq_sc_decode_q88",
 )
 
 _lib = None
@@ -62,6 +62,7 @@ def load():
     L.pq_decoder_get_option.argtypes = [vp, i]
     L.pq_sc_decode_f32.argtypes = [vp, vp, u32p, u32p, u32p, i, vp]
     L.pq_sc_decode_f32_dump.argtypes = [vp, vp, u32p, u32p, u32p, vp, i, vp]
+    L.pq_sc_decode_q88.argtypes = [vp, vp, u32p, u32p, u32p, i, vp]
     L.pq_sc_decode_bsc.argtypes = [vp, u32p, ctypes.c_float, u32p, u32p, u32p, i, vp]
     L.pq_polar_transform.argtypes = [u32p, u32p, i, i, vp]
     L.pq_decoder_workspace_bytes.argtypes = [vp]

@@ -331,7 +331,8 @@ enum : uint8_t { NT_MIXED = 0, NT_RATE0 = 1, NT_RATE1 = 2, NT_REP = 3 };
 struct DecParams {
     int n, log2S, plain, frames;
     uint32_t N, S, wpf;          // block length, shared sub-tree width, words per frame
-    const float *llr;            // [F][N] fp32 channel LLRs (or null when ybits)
+    const float *llr;            // [F][N] fp32 channel LLRs (or null when ybits / llr16)
+    const short *llr16;          // [F][N] Q8.8 raw channel codes (fixed mode), or null
     const uint32_t *ybits;       // [F][wpf] BSC received bits (or null)
     float mag;                   // BSC LLR magnitude
     const uint32_t *cw;          // [F][wpf] coset words c = T(v & mask), or null
@@ -351,6 +352,7 @@ enum { PR_UP_F = 0, PR_UP_G, PR_UP_OTHER, PR_SM_F, PR_SM_G, PR_SM_OTHER, PR_WARP
 
 struct FrameCtx {
     const float *llr;
+    const short *l16;
     const uint32_t *y, *cw;
     float *scr;
     uint32_t *X;
@@ -364,8 +366,13 @@ __device__ __forceinline__ float chan_load(const DecParams &p, const FrameCtx &f
         const uint32_t y = (fc.y[i >> 5] >> (i & 31)) & 1u;
         return (y ^ c) ? -p.mag : p.mag;  // p.mag is pre-quantised in fixed mode
     }
-    float v = fc.llr[i];
-    if (p.fixed) v = fminf(fmaxf(rintf(v * 256.0f), -Q_MAX), Q_MAX);
+    float v;
+    if (fc.l16) {
+        v = (float)fc.l16[i];  // already a Q8.8 code (|raw| <= 32767 by contract)
+    } else {
+        v = fc.llr[i];
+        if (p.fixed) v = fminf(fmaxf(rintf(v * 256.0f), -Q_MAX), Q_MAX);
+    }
     return c ? -v : v;
 }
 
@@ -382,8 +389,13 @@ __device__ __forceinline__ float4 chan_load4(const DecParams &p, const FrameCtx 
         v.w = (y4 & 8u) ? -p.mag : p.mag;
         return v;
     }
-    v = __ldg(reinterpret_cast<const float4 *>(fc.llr + i));
-    if (p.fixed) {
+    if (fc.l16) {
+        const short4 q = __ldg(reinterpret_cast<const short4 *>(fc.l16 + i));
+        v = make_float4((float)q.x, (float)q.y, (float)q.z, (float)q.w);
+    } else {
+        v = __ldg(reinterpret_cast<const float4 *>(fc.llr + i));
+    }
+    if (p.fixed && !fc.l16) {
         v.x = fminf(fmaxf(rintf(v.x * 256.0f), -Q_MAX), Q_MAX);
         v.y = fminf(fmaxf(rintf(v.y * 256.0f), -Q_MAX), Q_MAX);
         v.z = fminf(fmaxf(rintf(v.z * 256.0f), -Q_MAX), Q_MAX);
@@ -1148,6 +1160,7 @@ __device__ __forceinline__ void fence_proxy_async()
 // left-child partial sums (g-steps).  Offsets are element indices.
 struct UpSrc {
     const float *a, *b;          // stage or fp32 channel halves (null: BSC bits)
+    const short *a16, *b16;      // Q8.8 channel halves (fixed mode, int16 input), or null
     const uint32_t *ya, *yb;     // BSC received-bit halves (or null)
     const uint32_t *ca, *cb;     // coset words of the halves (or null)
     const uint32_t *xl;          // g-step: left-child partial sums (bit e of the range), or null
@@ -1169,6 +1182,7 @@ __device__ __forceinline__ void ring_issue(const Ring &r, const UpSrc &u, uint32
     const uint32_t C = r.C, wb = C / 8;  // bytes of C bits
     uint32_t bytes = 0;
     if (u.a) bytes += 8 * C;
+    if (u.a16) bytes += 4 * C;
     if (u.ya) bytes += 2 * wb;
     if (u.ca) bytes += 2 * wb;
     if (u.xl) bytes += wb;
@@ -1176,6 +1190,10 @@ __device__ __forceinline__ void ring_issue(const Ring &r, const UpSrc &u, uint32
     if (u.a) {
         bulk_g2s(st, u.a + e0, 4 * C, &r.bar[s]);
         bulk_g2s(st + 4 * C, u.b + e0, 4 * C, &r.bar[s]);
+    }
+    if (u.a16) {
+        bulk_g2s(st, u.a16 + e0, 2 * C, &r.bar[s]);
+        bulk_g2s(st + 4 * C, u.b16 + e0, 2 * C, &r.bar[s]);
     }
     if (u.ya) {
         bulk_g2s(st + 8 * C, u.ya + e0 / 32, wb, &r.bar[s]);
@@ -1206,9 +1224,14 @@ __device__ __forceinline__ float4 ring_val4(const DecParams &p, const UpSrc &u, 
         v.w = (y4 & 8u) ? -p.mag : p.mag;
         return v;
     }
-    v = *reinterpret_cast<const float4 *>(st + (size_t)half * 4 * C + 4 * k);
+    if (u.a16) {
+        const short4 q = *reinterpret_cast<const short4 *>(st + (size_t)half * 4 * C + 2 * k);
+        v = make_float4((float)q.x, (float)q.y, (float)q.z, (float)q.w);
+    } else {
+        v = *reinterpret_cast<const float4 *>(st + (size_t)half * 4 * C + 4 * k);
+    }
     if (u.chan) {
-        if (p.fixed) {  // channel LLRs -> Q8.8 codes on load, as chan_load4
+        if (p.fixed && !u.a16) {  // channel LLRs -> Q8.8 codes on load, as chan_load4
             v.x = fminf(fmaxf(rintf(v.x * 256.0f), -Q_MAX), Q_MAX);
             v.y = fminf(fmaxf(rintf(v.y * 256.0f), -Q_MAX), Q_MAX);
             v.z = fminf(fmaxf(rintf(v.z * 256.0f), -Q_MAX), Q_MAX);
@@ -1318,6 +1341,7 @@ __global__ void __launch_bounds__(256, 2) sc_decode_kernel(DecParams p)
     __shared__ float cl_slot;
     FrameCtx fc;
     fc.llr = p.llr ? p.llr + (size_t)frame * N : nullptr;
+    fc.l16 = p.llr16 ? p.llr16 + (size_t)frame * N : nullptr;
     fc.y = p.ybits ? p.ybits + (size_t)frame * p.wpf : nullptr;
     fc.cw = p.cw ? p.cw + (size_t)frame * p.wpf : nullptr;
     fc.scr = p.scr ? p.scr + (size_t)frame * N : nullptr;
@@ -1551,7 +1575,10 @@ __global__ void __launch_bounds__(256, 2) sc_decode_kernel(DecParams p)
                 memset(&u, 0, sizeof u);
                 if (ch0) {
                     u.chan = true;
-                    if (fc.llr) {
+                    if (fc.l16) {
+                        u.a16 = fc.l16;
+                        u.b16 = fc.l16 + H;
+                    } else if (fc.llr) {
                         u.a = fc.llr;
                         u.b = fc.llr + H;
                     } else {
@@ -1664,7 +1691,10 @@ __global__ void __launch_bounds__(256, 2) sc_decode_kernel(DecParams p)
                 memset(&u, 0, sizeof u);
                 if (ch0) {
                     u.chan = true;
-                    if (fc.llr) {
+                    if (fc.l16) {
+                        u.a16 = fc.l16;
+                        u.b16 = fc.l16 + W;
+                    } else if (fc.llr) {
                         u.a = fc.llr;
                         u.b = fc.llr + W;
                     } else {
@@ -2219,13 +2249,13 @@ int pq_polar_transform(const uint32_t *in, uint32_t *out, int n, int frames, voi
 
 static int decode_impl(pq_decoder *h, const float *llr, const uint32_t *ybits, float mag,
                        const uint32_t *frozen_u, uint32_t *u_hat, uint32_t *x_hat, float *dump,
-                       int frames, void *stream)
+                       int frames, void *stream, const short *llr16 = nullptr)
 {
     if (!h) return set_err(-1, "handle is NULL");
     if (!h->have_mask) return set_err(-1, "frozen mask not set (pq_decoder_set_frozen_mask)");
     if (frames < 0 || frames > h->max_frames)
         return set_err(-1, "frames=%d outside [0, max_frames=%d]", frames, h->max_frames);
-    if (!llr && !ybits) return set_err(-1, "no channel input");
+    if (!llr && !ybits && !llr16) return set_err(-1, "no channel input");
     if (frames == 0) return 0;
     cudaStream_t st = (cudaStream_t)stream;
     CUDA_TRY(cudaSetDevice(h->device));
@@ -2247,6 +2277,7 @@ static int decode_impl(pq_decoder *h, const float *llr, const uint32_t *ybits, f
     p.S = 1u << p.log2S;
     p.wpf = h->wpf;
     p.llr = llr;
+    p.llr16 = llr16;
     p.ybits = ybits;
     p.mag = mag;
     p.cw = cw;
@@ -2311,6 +2342,16 @@ int pq_sc_decode_f32(pq_decoder *h, const float *llr, const uint32_t *frozen_u, 
     if (frames == 0 && h) return 0;
     if (!llr) return set_err(-1, "llr is NULL");
     return decode_impl(h, llr, nullptr, 0.0f, frozen_u, u_hat, x_hat, nullptr, frames, stream);
+}
+
+int pq_sc_decode_q88(pq_decoder *h, const int16_t *llr_q88, const uint32_t *frozen_u, uint32_t *u_hat,
+                     uint32_t *x_hat, int frames, void *stream)
+{
+    if (frames == 0 && h) return 0;
+    if (!llr_q88) return set_err(-1, "llr_q88 is NULL");
+    if (h && h->fmode != PQ_F_FIXED) return set_err(-1, "pq_sc_decode_q88 needs a PQ_F_FIXED decoder");
+    return decode_impl(h, nullptr, nullptr, 0.0f, frozen_u, u_hat, x_hat, nullptr, frames, stream,
+                       reinterpret_cast<const short *>(llr_q88));
 }
 
 int pq_sc_decode_f32_dump(pq_decoder *h, const float *llr, const uint32_t *frozen_u, uint32_t *u_hat,

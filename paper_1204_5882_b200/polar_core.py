@@ -187,6 +187,24 @@ class ScDecoder:
         _lib.check(rc, "pq_sc_decode_f32")
         return u_hat, x_hat
 
+    def decode_q88(self, llr_q88, frozen_u=None, u_hat=None, x_hat=None, want_u=True, want_x=False,
+                   stream=None):
+        """SPEC.md:250 sc_decode_fixed on the device: llr_q88 is a contiguous
+        [F, N] int16 CUDA tensor of saturating Q8.8 raw codes (quantize_q88);
+        fixed-point decoders only."""
+        if not (llr_q88.is_cuda and llr_q88.dtype == torch.int16 and llr_q88.is_contiguous()
+                and llr_q88.dim() == 2):
+            raise ValueError("llr_q88 must be a contiguous [frames, N] int16 CUDA tensor")
+        F = llr_q88.shape[0]
+        if llr_q88.shape[1] != self.N:
+            raise ValueError(f"llr length {llr_q88.shape[1]} != N = {self.N}")
+        u_hat, x_hat = self._outs(F, u_hat, x_hat, want_u, want_x)
+        _check_words(frozen_u, F, self.wpf, "frozen_u")
+        rc = _lib.load().pq_sc_decode_q88(self._h, _ptr(llr_q88), _ptr(frozen_u), _ptr(u_hat), _ptr(x_hat),
+                                          F, _stream_ptr(stream))
+        _lib.check(rc, "pq_sc_decode_q88")
+        return u_hat, x_hat
+
     def decode_bsc(self, y_words, llr_mag: float, frozen_u=None, u_hat=None, x_hat=None,
                    want_u=True, want_x=False, frames=None, stream=None):
         """Fused BSC front end: y_words [F, N/32] int32 received bits."""
@@ -314,13 +332,26 @@ def quantize_q88(llrs) -> np.ndarray:
 
 def sc_decode_fixed(code: PolarCode, llrs_fixed, frozen_values) -> np.ndarray:
     """SC decode of raw Q8.8 LLRs (int16 codes) with saturating
-    fixed-point arithmetic and the phi table, on the GPU (bit-exact with the
-    fixed-point oracle).  Raw codes travel as fp32 raw/256 (exact) and are
-    re-quantised exactly on load."""
+    fixed-point arithmetic and the table boxplus, on the GPU (bit-exact with
+    the fixed-point oracle); the codes go to the device as int16."""
     raw = np.asarray(llrs_fixed)
     if raw.dtype.kind not in "iu":
         raise ValueError("llrs_fixed must be integer Q8.8 codes (see quantize_q88)")
-    return sc_decode(code, raw.astype(np.float32) / np.float32(256.0), frozen_values, f_mode="fixed")
+    if raw.shape[-1] != code.block_size:
+        raise ValueError(f"llrs length {raw.shape[-1]} != 2^n = {code.block_size}")
+    dev = _require_cuda()
+    batch = np.clip(raw.reshape(-1, code.block_size), -32767, 32767).astype(np.int16)
+    full = scatter_frozen_values(code, frozen_values).reshape(-1, code.block_size)
+    if full.shape[0] not in (1, batch.shape[0]):
+        raise ValueError("frozen_values batch does not match llrs")
+    if full.shape[0] == 1 and batch.shape[0] > 1:
+        full = np.repeat(full, batch.shape[0], axis=0)
+    dec = _cached_decoder(code, batch.shape[0], "fixed")
+    u, _ = dec.decode_q88(torch.from_numpy(batch).to(dev),
+                          torch.from_numpy(pack_bits(full).view(np.int32).copy()).to(dev))
+    torch.cuda.current_stream().synchronize()
+    out = unpack_bits(u.cpu().numpy().view(np.uint32), code.block_size)
+    return out.reshape(raw.shape).astype(np.uint8)
 
 
 def sc_decode(code: PolarCode, llrs, frozen_values, f_mode: str = "exact") -> np.ndarray:

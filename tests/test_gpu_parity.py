@@ -570,3 +570,57 @@ def test_cluster_auto_c5_shape_matches_single_cta(cuda):
         u, _ = dec.decode(to_dev(llr, cuda), words_dev(u_true, cuda))
         outs.append(u.cpu().numpy())
     assert np.array_equal(outs[0], outs[1])
+
+
+@pytest.mark.parametrize("bsc", [True, False])
+def test_pipelined_decoder_matches_direct(cuda, bsc):
+    """pipeline.PipelinedDecoder: several host batches in flight on three streams
+    give the same u-hat as one direct decode per batch."""
+    import torch
+    from paper_1204_5882_b200.pipeline import PipelinedDecoder
+    if "c1" not in K.available_configs():
+        pytest.skip("c1 not built")
+    cfg, code, x, u_true, llr = config_batch("c1", 32)
+    N = code.block_size
+    dec = ScDecoder(code, max_frames=16, f_mode="fixed")
+    mag = np.float32(cfg.channel.llr_magnitude) if bsc else None
+    pipe = PipelinedDecoder(dec, 16, bsc_llr_mag=mag)
+    batches = []
+    for b in range(5):  # batches 0..4 over frames [0,16), [16,32), [0,16), ...
+        sl = slice(16 * (b % 2), 16 * (b % 2) + 16)
+        if bsc:
+            y = np.array([C.frame(cfg.channel, cfg.seed, j, N)[1] for j in range(sl.start, sl.stop)])
+            h_in = torch.from_numpy(pack_bits(y).view(np.int32).copy()).pin_memory()
+        else:
+            h_in = torch.from_numpy(np.ascontiguousarray(llr[sl])).pin_memory()
+        h_fz = torch.from_numpy(pack_bits(u_true[sl]).view(np.int32).copy()).pin_memory()
+        h_out = torch.empty((16, N // 32), dtype=torch.int32).pin_memory()
+        pipe.submit(h_in, h_fz, h_out)
+        batches.append((sl, h_out))
+    pipe.synchronize()
+    ref = ScDecoder(code, max_frames=32, f_mode="fixed")
+    u_ref, _ = ref.decode(to_dev(llr, cuda), words_dev(u_true, cuda))
+    u_ref = from_words(u_ref, N)
+    for sl, h_out in batches:
+        assert np.array_equal(unpack_bits(h_out.numpy().view(np.uint32), N), u_ref[sl])
+
+
+def test_q88_input_matches_fp32_input(cuda):
+    """pq_sc_decode_q88 (int16 Q8.8 codes) = the fixed decoder on fp32 LLRs that
+    quantise to the same codes, on all five paths the channel reaches (root
+    f/g steps through the TMA ring at n = 16, S = 2^11; a small block whose root
+    is in the warp band)."""
+    import torch
+    rng = np.random.default_rng(77)
+    for n, lg in ((16, 11), (9, 0), (14, 0)):
+        code = random_code(n, 0.45, rng)
+        N, F = 1 << n, 3
+        llr = rng.normal(0.8, 2.5, (F, N)).astype(np.float32)
+        fz = rng.integers(0, 2, (F, N)).astype(np.uint8)
+        raw = O.quantize_q88(llr)
+        ref = fixed_oracle_batch(code, raw, fz)
+        dec = ScDecoder(code, max_frames=F, f_mode="fixed", subtree_log2=lg)
+        u, _ = dec.decode_q88(torch.from_numpy(raw).to(cuda), words_dev(fz, cuda))
+        assert np.array_equal(from_words(u, N), ref)
+    with pytest.raises(ValueError):
+        ScDecoder(code, max_frames=F, f_mode="exact").decode_q88(torch.from_numpy(raw).to(cuda))
