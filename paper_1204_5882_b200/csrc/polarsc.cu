@@ -687,7 +687,10 @@ __device__ __noinline__ uint32_t dec8(float v, const TypeBits T, int h, const No
     UB_BEGIN();
     const unsigned FULL = 0xffffffffu;
     uint32_t bits;
-    if (!plain && tget(T, h) == NT_MIXED && w8_fast<FM>(v, (T.leaf >> (8 * (h - 4))) & 0xffu, bits)) {
+#ifndef PQ_W8_PATTERNS
+#define PQ_W8_PATTERNS 1
+#endif
+    if (PQ_W8_PATTERNS && !plain && tget(T, h) == NT_MIXED && w8_fast<FM>(v, (T.leaf >> (8 * (h - 4))) & 0xffu, bits)) {
         UB_END(4);
         return bits;
     }
@@ -959,6 +962,27 @@ __device__ __forceinline__ void walk_leaf32(const WalkCtx &c, uint32_t lh, uint3
 }
 
 template <int FM, bool PLAIN, int W>
+__device__ __forceinline__ void walk_node(const WalkCtx &c, uint32_t lh, uint32_t pos);
+
+#ifndef PQ_WALK_NOINLINE
+#define PQ_WALK_NOINLINE 0
+#endif
+// a child of the warp walk: one out-of-line copy per width (code size: the
+// inlined recursion duplicates every level 2^k times)
+template <int FM, bool PLAIN, int W>
+__device__ __noinline__ void walk_child_ool(const WalkCtx c, uint32_t lh, uint32_t pos)
+{
+    walk_node<FM, PLAIN, W>(c, lh, pos);
+}
+template <int FM, bool PLAIN, int W>
+__device__ __forceinline__ void walk_child(const WalkCtx &c, uint32_t lh, uint32_t pos)
+{
+    if constexpr (W == 32) walk_leaf32<FM, PLAIN>(c, lh, pos);
+    else if constexpr (PQ_WALK_NOINLINE && !PLAIN) walk_child_ool<FM, PLAIN, W>(c, lh, pos);
+    else walk_node<FM, PLAIN, W>(c, lh, pos);
+}
+
+template <int FM, bool PLAIN, int W>
 __device__ __forceinline__ void walk_node(const WalkCtx &c, uint32_t lh, uint32_t pos)
 {
     constexpr uint32_t V = W / 32, H = W / 2, Vh = V / 2;
@@ -1028,8 +1052,7 @@ __device__ __forceinline__ void walk_node(const WalkCtx &c, uint32_t lh, uint32_
             }
         }
         __syncwarp();
-        if constexpr (H == 32) walk_leaf32<FM, PLAIN>(c, 2 * lh, pos);
-        else walk_node<FM, PLAIN, H>(c, 2 * lh, pos);
+        walk_child<FM, PLAIN, H>(c, 2 * lh, pos);
     }
     // ---- right child: g-step with the left child's partial sums
     if (!PLAIN && c.ty[2 * lh + 1] == NT_RATE0) {
@@ -1054,8 +1077,7 @@ __device__ __forceinline__ void walk_node(const WalkCtx &c, uint32_t lh, uint32_
             }
         }
         __syncwarp();
-        if constexpr (H == 32) walk_leaf32<FM, PLAIN>(c, 2 * lh + 1, pos + H);
-        else walk_node<FM, PLAIN, H>(c, 2 * lh + 1, pos + H);
+        walk_child<FM, PLAIN, H>(c, 2 * lh + 1, pos + H);
     }
     // ---- partial sums of this node: (xl ^ xr, xr)
     if (lane < (int)Vh) xw[lane] ^= xw[Vh + lane];
@@ -1091,6 +1113,163 @@ __device__ __noinline__ void warp_walk(float *st_end, uint32_t *xs, const uint8_
     UB_BEGIN();
     if (plain_i) walk_root<FM, true>(c, W, lh, pos);
     else walk_root<FM, false>(c, W, lh, pos);
+    UB_END(2);
+}
+
+// ---- register-resident warp walk (SSC path; plain mode and the stage dump
+// keep warp_walk).  Lane l holds elements l + 32q of every node of width
+// W >= 32 in registers; f/g steps are in-lane (no shared-memory round trip,
+// no __syncwarp); partial sums travel as warp-uniform words returned by the
+// children.  Node types of the walk's upper levels (widths W0 .. 32 below the
+// root, relative heap positions 1..31) are two uniform bit masks built once
+// per walk; REL (the relative heap position) is a template parameter, so
+// every type test is a shift by a constant.
+struct W2Ctx {
+    const uint8_t *ty;  // S-local heap-order types (shared memory)
+    uint32_t root;      // S-local heap index of the walk root
+    uint32_t wb0, wb1;  // type bits of relative heap positions 1..31
+    int k32;            // relative depth of the width-32 level below the root
+};
+template <int REL>
+__device__ __forceinline__ uint32_t w2_type(const W2Ctx &c)
+{
+    return ((c.wb0 >> REL) & 1u) | (((c.wb1 >> REL) & 1u) << 1);
+}
+
+template <int FM, int W, int REL>
+__device__ __forceinline__ void w2_node(const float (&x)[W / 32], const W2Ctx &c, uint32_t (&xo)[W / 32]);
+
+// width-32 child at relative position REL: TypeBits from shared memory, then
+// the register engine (lane l = element l)
+template <int FM, int REL>
+__device__ __forceinline__ uint32_t w2_leaf(float v, const W2Ctx &c)
+{
+    const uint32_t lh = (c.root << c.k32) + (uint32_t)REL - (1u << c.k32);
+    const TypeBits T = load_typebits(c.ty, lh, 32, false);
+    NodePos np;
+    np.dump = nullptr;
+    np.N = 0;
+    np.d = 0;
+    np.j = 0;
+    return dec32<FM, false>(v, T, np);
+}
+
+template <int FM, int H, int REL>
+__device__ __forceinline__ void w2_child(const float (&x)[H / 32], const W2Ctx &c, uint32_t (&xo)[H / 32])
+{
+    if constexpr (H == 32) xo[0] = w2_leaf<FM, REL>(x[0], c);
+    else w2_node<FM, H, REL>(x, c, xo);
+}
+
+template <int FM, int W, int REL>
+__device__ __forceinline__ void w2_node(const float (&x)[W / 32], const W2Ctx &c, uint32_t (&xo)[W / 32])
+{
+    constexpr int V = W / 32, Vh = V / 2;
+    const unsigned FULL = 0xffffffffu;
+    const int lane = threadIdx.x & 31;
+    const uint32_t t = w2_type<REL>(c);
+    if (t == NT_RATE0) {
+#pragma unroll
+        for (int q = 0; q < V; q++) xo[q] = 0u;
+        return;
+    }
+    if (t == NT_RATE1) {
+        uint32_t m = 0x7f800000u;
+#pragma unroll
+        for (int q = 0; q < V; q++) m = min(m, __float_as_uint(x[q]) & 0x7fffffffu);
+        m = __reduce_min_sync(FULL, m);
+        if (rate1_guard<FM>(__uint_as_float(m), ilog2((uint32_t)W))) {
+#pragma unroll
+            for (int q = 0; q < V; q++) xo[q] = __ballot_sync(FULL, x[q] < 0.0f);
+            return;
+        }
+    }
+    if (t == NT_REP) {
+        // SC's g-chain with zero partial sums, in SC's pairing order
+        float sm8[V];
+#pragma unroll
+        for (int q = 0; q < V; q++) sm8[q] = x[q];
+#pragma unroll
+        for (int hv = V / 2; hv >= 1; hv >>= 1)
+#pragma unroll
+            for (int q = 0; q < hv; q++) sm8[q] = qadd<FM>(sm8[q + hv], sm8[q]);
+        float s0 = sm8[0];
+#pragma unroll
+        for (int hh = 16; hh >= 1; hh >>= 1) s0 = qadd<FM>(__shfl_down_sync(FULL, s0, hh), s0);
+        const uint32_t bits = __shfl_sync(FULL, s0, 0) < 0.0f ? FULL : 0u;
+#pragma unroll
+        for (int q = 0; q < V; q++) xo[q] = bits;
+        return;
+    }
+    float ch[Vh];
+    uint32_t xl[Vh], xr[Vh];
+    if (w2_type<2 * REL>(c) == NT_RATE0) {
+#pragma unroll
+        for (int q = 0; q < Vh; q++) xl[q] = 0u;
+    } else {
+#pragma unroll
+        for (int q = 0; q < Vh; q++) ch[q] = pq_f<FM>(x[q], x[q + Vh]);
+        w2_child<FM, W / 2, 2 * REL>(ch, c, xl);
+    }
+    if (w2_type<2 * REL + 1>(c) == NT_RATE0) {
+#pragma unroll
+        for (int q = 0; q < Vh; q++) xr[q] = 0u;
+    } else {
+#pragma unroll
+        for (int q = 0; q < Vh; q++) ch[q] = pq_gt<FM>(x[q], x[q + Vh], (xl[q] >> lane) & 1u);
+        w2_child<FM, W / 2, 2 * REL + 1>(ch, c, xr);
+    }
+#pragma unroll
+    for (int q = 0; q < Vh; q++) {
+        xo[q] = xl[q] ^ xr[q];
+        xo[Vh + q] = xr[q];
+    }
+}
+
+template <int FM, int W>
+__device__ __forceinline__ void w2_root(const float *nd, uint32_t *xw, const W2Ctx &c)
+{
+    constexpr int V = W / 32;
+    const int lane = threadIdx.x & 31;
+    float x[V];
+    uint32_t xo[V];
+#pragma unroll
+    for (int q = 0; q < V; q++) x[q] = nd[32 * q + lane];
+    w2_node<FM, W, 1>(x, c, xo);
+#pragma unroll
+    for (int q = 0; q < V; q++)
+        if (lane == q) xw[q] = xo[q];
+    __syncwarp();
+}
+
+// the SSC warp walk from the stage buffer of the root (width W, 64..512)
+template <int FM>
+__device__ __noinline__ void warp_walk2(float *st_end, uint32_t *xs, const uint8_t *ty, uint32_t S, int dS, int d0,
+                                        uint32_t j0)
+{
+    const unsigned FULL = 0xffffffffu;
+    const int lane = threadIdx.x & 31;
+    const uint32_t W = S >> (d0 - dS);
+    const int e = d0 - dS;
+    W2Ctx c;
+    c.ty = ty;
+    c.root = (1u << e) + (j0 & ((1u << e) - 1u));
+    c.k32 = ilog2(W) - 5;
+    // types of relative heap positions 1..31 down to the width-32 level
+    uint32_t tint = NT_MIXED;
+    if (lane >= 1) {
+        const int k = ilog2((uint32_t)lane);
+        if (k <= c.k32) tint = ty[(c.root << k) + (uint32_t)lane - (1u << k)];
+    }
+    c.wb0 = __ballot_sync(FULL, tint & 1u);
+    c.wb1 = __ballot_sync(FULL, tint & 2u);
+    const float *nd = st_end - 2 * W;
+    uint32_t *xw = xs + (((j0 * W) & (S - 1)) >> 5);
+    UB_BEGIN();
+    if (W == 512) w2_root<FM, 512>(nd, xw, c);
+    else if (W == 256) w2_root<FM, 256>(nd, xw, c);
+    else if (W == 128) w2_root<FM, 128>(nd, xw, c);
+    else w2_root<FM, 64>(nd, xw, c);
     UB_END(2);
 }
 
@@ -1505,7 +1684,13 @@ __global__ void __launch_bounds__(256, 2) sc_decode_kernel(DecParams p)
                             for (uint32_t i = tid & 31; i < W; i += 32) dst[i] = chan_load(p, fc, i);
                             __syncwarp();
                         }
-                        warp_walk<FM>(sm.st + 2 * S, sm.xs, sm.ty, fc.dump, N, S, dS, wc.jS, p.plain, d, j);
+#ifndef PQ_WALK2
+#define PQ_WALK2 1
+#endif
+                        if (PQ_WALK2 && !p.plain && fc.dump == nullptr && W >= 64)
+                            warp_walk2<FM>(sm.st + 2 * S, sm.xs, sm.ty, S, dS, d, j);
+                        else
+                            warp_walk<FM>(sm.st + 2 * S, sm.xs, sm.ty, fc.dump, N, S, dS, wc.jS, p.plain, d, j);
                     } else {
                         const float *src = chan ? nullptr : stage_ptr(p, fc, sm, W);
                         warp_small<FM>(src, chan, p, fc, lh, wc, sm.xs, pos, (int)W);

@@ -21,10 +21,11 @@ from paper_1204_5882_b200.polar_core import ScDecoder, pack_bits, polar_transfor
 ap = argparse.ArgumentParser()
 ap.add_argument("--config", default="c3")
 ap.add_argument("--fmode", default="fixed")
+ap.add_argument("--frames", type=int, default=0)
 a = ap.parse_args()
 cfg = K.CONFIGS[a.config]
 code = K.load_config(a.config)
-F = cfg.frames_per_gpu
+F = a.frames or cfg.frames_per_gpu
 x, llr, _ = gen_frames(cfg, code.block_size, 0, F)
 dev = torch.device("cuda", 0)
 u = polar_transform_words(torch.from_numpy(pack_bits(x).view(np.int32).copy()).to(dev), code.n)
