@@ -131,6 +131,24 @@ int pq_sc_decode_bsc(pq_decoder *h, const uint32_t *y_bits, float llr_mag,
  * also alice_disclose's u = polar_transform(x).             */
 int pq_polar_transform(const uint32_t *in, uint32_t *out, int n, int frames, void *stream);
 
+/* Verification step of bob_decode ("returns Verified if
+ * hash(x_hat) equals verification_hash, else Discarded").  The hash is
+ * XXH64 ("a fixed, well-known 64-bit non-cryptographic hash,
+ * seed-keyed per session") of each frame's packed words read as
+ * little-endian bytes (4 * max(1, N/32) bytes), seed = the session key.
+ * Replaces: the hash(...) inside alice_disclose and
+ * bob_decode's comparison, batched over frames on the
+ * device.
+ *   pq_hash_frames:   hash_out[f] = XXH64(frame f)
+ *   pq_verify_frames: verified[f] = (XXH64(frame f) == expect[f]) (nullable),
+ *                     *n_discarded += #mismatches (device counter, nullable)
+ *   pq_xxh64:         the same hash on the host (CPU, any byte string).   */
+int pq_hash_frames(const uint32_t *x_words, int n, int frames, uint64_t seed, uint64_t *hash_out,
+                   void *stream);
+int pq_verify_frames(const uint32_t *x_words, int n, int frames, uint64_t seed, const uint64_t *expect,
+                     uint8_t *verified, unsigned int *n_discarded, void *stream);
+uint64_t pq_xxh64(const void *data, size_t len, uint64_t seed);
+
 /* Copy the per-frame cycle profile of the last decode (PQ_OPT_PROFILE=1):
  * out[frame][PQ_PROF_SLOTS] = {upper f, upper g, upper other, shared f,
  * shared g, shared other, warp sub-trees, type staging, rate-1, total,

@@ -71,8 +71,22 @@ def lib():
         L.orc_sc_decode_fixed.argtypes = [ctypes.c_int, u8p, i16p, u8p, u8p, ctypes.c_void_p, ctypes.c_void_p,
                                           ctypes.c_void_p]
         L.orc_fmag_f64_vec.argtypes = [f64p, f64p, f64p, ctypes.c_size_t]
+        L.orc_xxh64.argtypes = [ctypes.c_char_p, ctypes.c_size_t, ctypes.c_uint64]
+        L.orc_xxh64.restype = ctypes.c_uint64
         _lib = L
     return _lib
+
+
+# --------------------------------------------------------------------------
+# verification hash (XXH64, seed-keyed; sc_oracle.c orc_xxh64)
+
+def xxh64(data: bytes, seed: int = 0) -> int:
+    return int(lib().orc_xxh64(bytes(data), len(data), seed & (2 ** 64 - 1)))
+
+
+def block_hash_words(words, seed: int = 0) -> int:
+    """XXH64 of one frame's packed uint32 words as little-endian bytes."""
+    return xxh64(np.ascontiguousarray(np.asarray(words, dtype="<u4")).tobytes(), seed)
 
 
 # --------------------------------------------------------------------------

@@ -474,3 +474,73 @@ void orc_fmag_f64_vec(const double *a, const double *b, double *out, size_t coun
 {
     for (size_t i = 0; i < count; i++) out[i] = orc_fmag_f64(a[i], b[i]);
 }
+
+/* ---------------------------------------------------------------------------
+ * Verification hash of bob_decode (the DESIGN DECISIONS
+ * ledger, fixes "a fixed, well-known 64-bit non-cryptographic
+ * hash, seed-keyed per session"): XXH64 of the packed block bytes (bit i of
+ * the block = byte i>>3, bit i&7, LSB-first -- the PQCT/word packing), seed =
+ * the session key.  A plain restatement of the published XXH64 algorithm
+ * (xxHash specification, "XXH64 algorithm description"): four lane
+ * accumulators over 32-byte stripes, merge, length, 8/4/1-byte tail,
+ * avalanche.  Byte-serial and independent of the product's CUDA/C++ code. */
+#define XP1 0x9E3779B185EBCA87ull
+#define XP2 0xC2B2AE3D27D4EB4Full
+#define XP3 0x165667B19E3779F9ull
+#define XP4 0x85EBCA77C2B2AE63ull
+#define XP5 0x27D4EB2F165667C5ull
+static inline uint64_t xrotl(uint64_t x, int r) { return (x << r) | (x >> (64 - r)); }
+static inline uint64_t xrd64(const uint8_t *p)
+{
+    uint64_t v = 0;
+    for (int i = 7; i >= 0; i--) v = (v << 8) | p[i];
+    return v;
+}
+static inline uint64_t xrd32(const uint8_t *p) { return (uint64_t)p[0] | ((uint64_t)p[1] << 8) | ((uint64_t)p[2] << 16) | ((uint64_t)p[3] << 24); }
+static inline uint64_t xround(uint64_t acc, uint64_t in) { return xrotl(acc + in * XP2, 31) * XP1; }
+static inline uint64_t xmerge(uint64_t h, uint64_t v) { return (h ^ xround(0, v)) * XP1 + XP4; }
+
+uint64_t orc_xxh64(const uint8_t *p, size_t len, uint64_t seed)
+{
+    const uint8_t *end = p + len;
+    uint64_t h;
+    if (len >= 32) {
+        uint64_t v1 = seed + XP1 + XP2, v2 = seed + XP2, v3 = seed, v4 = seed - XP1;
+        while (end - p >= 32) {
+            v1 = xround(v1, xrd64(p));
+            v2 = xround(v2, xrd64(p + 8));
+            v3 = xround(v3, xrd64(p + 16));
+            v4 = xround(v4, xrd64(p + 24));
+            p += 32;
+        }
+        h = xrotl(v1, 1) + xrotl(v2, 7) + xrotl(v3, 12) + xrotl(v4, 18);
+        h = xmerge(h, v1);
+        h = xmerge(h, v2);
+        h = xmerge(h, v3);
+        h = xmerge(h, v4);
+    } else {
+        h = seed + XP5;
+    }
+    h += (uint64_t)len;
+    while (end - p >= 8) {
+        h ^= xround(0, xrd64(p));
+        h = xrotl(h, 27) * XP1 + XP4;
+        p += 8;
+    }
+    if (end - p >= 4) {
+        h ^= xrd32(p) * XP1;
+        h = xrotl(h, 23) * XP2 + XP3;
+        p += 4;
+    }
+    while (p < end) {
+        h ^= (uint64_t)(*p) * XP5;
+        h = xrotl(h, 11) * XP1;
+        p++;
+    }
+    h ^= h >> 33;
+    h *= XP2;
+    h ^= h >> 29;
+    h *= XP3;
+    h ^= h >> 32;
+    return h;
+}

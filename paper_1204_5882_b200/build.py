@@ -12,6 +12,7 @@ import sys
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 SRC = os.path.join(HERE, "csrc", "polarsc.cu")
+SRCS = [SRC, os.path.join(HERE, "csrc", "verify.cu")]
 OUT = os.path.join(HERE, "libpolarsc.so")
 INCLUDE = os.path.join(os.path.dirname(HERE), "include")
 
@@ -34,10 +35,10 @@ def nvcc() -> str:
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
-    deps = [SRC, os.path.join(INCLUDE, "polarsc.h")]
+    deps = [*SRCS, os.path.join(INCLUDE, "polarsc.h")]
     if not force and os.path.exists(OUT) and all(os.path.getmtime(OUT) >= os.path.getmtime(d) for d in deps):
         return OUT
-    cmd = [nvcc(), *NVCC_FLAGS, "-o", OUT + ".tmp", SRC]
+    cmd = [nvcc(), *NVCC_FLAGS, "-o", OUT + ".tmp", *SRCS]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
         print(" ".join(cmd), file=sys.stderr)

@@ -2227,6 +2227,9 @@ static int ensure_fixed_tables()
     return 0;
 }
 
+// error text for the other translation units of the library (verify.cu)
+int pq_set_error_text(int code, const char *msg) { return set_err(code, "%s", msg); }
+
 extern "C" {
 
 const char *pq_last_error(void) { return g_last_error.c_str(); }

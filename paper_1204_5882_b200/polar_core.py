@@ -281,6 +281,43 @@ def polar_transform_words(words, n: int, out=None, stream=None):
     return out
 
 
+def hash_frames(x_words, n: int, key: int = 0, out=None, stream=None):
+    """XXH64 (seed = key) of every frame's packed words on the device:
+    [F, N/32] int32 -> [F] int64 (the uint64 hash bits)."""
+    _require_cuda()
+    F = x_words.shape[0] if x_words.dim() == 2 else 1
+    _check_words(x_words, F, words_per_frame(n), "x_words")
+    if out is None:
+        out = torch.empty(F, dtype=torch.int64, device=x_words.device)
+    rc = _lib.load().pq_hash_frames(_ptr(x_words), n, F, key & (2 ** 64 - 1), _ptr(out), _stream_ptr(stream))
+    _lib.check(rc, "pq_hash_frames")
+    return out
+
+
+def verify_frames(x_words, n: int, expect, key: int = 0, verified=None, n_discarded=None, stream=None):
+    """bob_decode's verification on the device: verified[f]
+    = XXH64(x_hat[f], key) == expect[f] (uint8), and the discarded count is
+    added to n_discarded (int32 [1] device tensor) when given."""
+    _require_cuda()
+    F = x_words.shape[0] if x_words.dim() == 2 else 1
+    _check_words(x_words, F, words_per_frame(n), "x_words")
+    if not (expect.is_cuda and expect.dtype == torch.int64 and expect.numel() >= F):
+        raise ValueError("expect must be an int64 CUDA tensor of >= frames hashes")
+    if verified is None:
+        verified = torch.empty(F, dtype=torch.uint8, device=x_words.device)
+    rc = _lib.load().pq_verify_frames(_ptr(x_words), n, F, key & (2 ** 64 - 1), _ptr(expect), _ptr(verified),
+                                      _ptr(n_discarded) if n_discarded is not None else None,
+                                      _stream_ptr(stream))
+    _lib.check(rc, "pq_verify_frames")
+    return verified
+
+
+def block_hash_host(x_words: np.ndarray, key: int = 0) -> int:
+    """The same XXH64 on the host (no GPU needed), over packed words."""
+    data = np.ascontiguousarray(np.asarray(x_words, dtype="<u4")).tobytes()
+    return int(_lib.load().pq_xxh64(data, len(data), key & (2 ** 64 - 1)))
+
+
 def polar_transform(u) -> np.ndarray:
     """u (length 2^n bits, or [F, 2^n]) -> x, on the GPU."""
     dev = _require_cuda()
