@@ -149,6 +149,22 @@ int pq_verify_frames(const uint32_t *x_words, int n, int frames, uint64_t seed, 
                      uint8_t *verified, unsigned int *n_discarded, void *stream);
 uint64_t pq_xxh64(const void *data, size_t len, uint64_t seed);
 
+/* Density evolution on the GPU (the construction service's hot loop,
+ * SURVEY.md 8(f) f2).  Replaces: density_evolution(ch, n, quant, prune_z_eps,
+ * prune_i_eps, mass_floor) (construction.py:313-391) with its f/g transforms
+ * (_f_scatter / f_self / g_self, construction.py:138-158, :206-248) and the
+ * pruned-subtree fill (construction.py:296-310).  The grid tables are the
+ * reference's own (_GridOps, construction.py:166-197), computed on the host
+ * and passed in: f_idx / f_whi are (bins-1)^2 row-major, z_weights / i_loss
+ * have bins-1 entries.  pq_de_run takes the base density (bins+1 slots:
+ * -inf, interior, +inf) and writes pe[2^n] (host memory); synchronous.     */
+typedef struct pq_de pq_de;
+int pq_de_create(pq_de **out, int bins, double z_lo_bound, const int32_t *f_idx, const double *f_whi,
+                 const double *z_weights, const double *i_loss, int device);
+int pq_de_run(pq_de *h, const double *base_density, int n, double prune_z_eps, double prune_i_eps,
+              double mass_floor, double *pe_out);
+int pq_de_destroy(pq_de *h);
+
 /* Copy the per-frame cycle profile of the last decode (PQ_OPT_PROFILE=1):
  * out[frame][PQ_PROF_SLOTS] = {upper f, upper g, upper other, shared f,
  * shared g, shared other, warp sub-trees, type staging, rate-1, total,

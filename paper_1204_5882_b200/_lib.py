@@ -36,7 +36,7 @@ EXPORTS = (
     "pq_polar_transform", "pq_decoder_workspace_bytes", "pq_decoder_last_launches",
     "pq_decoder_destroy", "pq_last_error", "pq_abi_version", "pq_decoder_read_profile",
     "pq_debug_fmag", "pq_decoder_last_ctas_per_frame", "pq_decoder_last_config", "pq_sc_decode_q88",
-    "pq_hash_frames", "pq_verify_frames", "pq_xxh64",
+    "pq_hash_frames", "pq_verify_frames", "pq_xxh64", "pq_de_create", "pq_de_run", "pq_de_destroy",
 )
 
 _lib = None
@@ -78,6 +78,10 @@ def load():
     L.pq_verify_frames.argtypes = [u32p, i, i, ctypes.c_uint64, vp, vp, vp, vp]
     L.pq_xxh64.argtypes = [ctypes.c_char_p, ctypes.c_size_t, ctypes.c_uint64]
     L.pq_xxh64.restype = ctypes.c_uint64
+    dbl = ctypes.c_double
+    L.pq_de_create.argtypes = [ctypes.POINTER(vp), i, dbl, vp, vp, vp, vp, i]
+    L.pq_de_run.argtypes = [vp, vp, i, dbl, dbl, dbl, vp]
+    L.pq_de_destroy.argtypes = [vp]
     L.pq_last_error.restype = ctypes.c_char_p
     L.pq_abi_version.restype = ctypes.c_int
     for name in EXPORTS:

@@ -12,7 +12,7 @@ import sys
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 SRC = os.path.join(HERE, "csrc", "polarsc.cu")
-SRCS = [SRC, os.path.join(HERE, "csrc", "verify.cu")]
+SRCS = [SRC, os.path.join(HERE, "csrc", "verify.cu"), os.path.join(HERE, "csrc", "de.cu")]
 OUT = os.path.join(HERE, "libpolarsc.so")
 INCLUDE = os.path.join(os.path.dirname(HERE), "include")
 

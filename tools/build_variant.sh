@@ -7,5 +7,5 @@ tmp="$ROOT/paper_1204_5882_b200/csrc/_variant_$2.cu"
 cp "$1" "$tmp"
 mkdir -p "$ROOT/variants"
 nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 --fmad=false -prec-div=true -ftz=false $EXTRA -I "$ROOT/include" \
-     -Xcompiler -fPIC -shared -cudart static -o "$ROOT/variants/$2.so" "$tmp" "$ROOT/paper_1204_5882_b200/csrc/verify.cu" || { rm -f "$tmp"; exit 1; }
+     -Xcompiler -fPIC -shared -cudart static -o "$ROOT/variants/$2.so" "$tmp" "$ROOT/paper_1204_5882_b200/csrc/verify.cu" "$ROOT/paper_1204_5882_b200/csrc/de.cu" || { rm -f "$tmp"; exit 1; }
 rm -f "$tmp"
