@@ -225,12 +225,15 @@ def run_reference(args, rank, world):
             times.append(dt)
     tot = sum(times)
     v = F * N * len(times) / tot / 1e6
-    line = {"metric": "SC-decoded Mbit/s", "value": round(v, 3), "unit": "Mbit/s", "n_gpus": 0,
+    line = {"metric": "SC-decoded Mbit/s", "value": round(v, 3), "unit": "Mbit/s", "n_gpus": args.gpus,
+            "host_only": True,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(1e3 * tot / len(times), 3),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "q8.8 (int16)" if prec == 16 else "f64",
             "data": "synthetic (reference channel model, seeded)", "impl": "reference",
-            "config": {"workload": cfg.desc, "key": args.config, "frames_per_step": F, "N": N, "f": args.fmode},
+            "config": {"workload": cfg.desc, "key": args.config, "frames_per_gpu": cfg.frames_per_gpu, "N": N,
+                       "rate": cfg.rate, "f": args.fmode, "frames_per_step": F,
+                       "parallelism": f"{threads} host threads on rank 0 (the reference's decoder is CPU-only)"},
             "cpu_baseline": {"value": round(v, 3), "unit": "Mbit/s", "cores": threads, "kind": "port",
                              "sample": f"{F} frames of {args.config} per step (one per thread), {what}"},
             "e2e": {"value": round(v, 3), "unit": "Mbit/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
