@@ -1497,9 +1497,17 @@ __device__ __forceinline__ float cluster_min(float m, float *slot, uint32_t K)
     return r;
 }
 
-template <int FM, bool CL>
+// DIAG = false: the production instantiation -- no plain-SC mode, stage dump
+// or cycle profile in the code at all (a smaller, branch-free main loop: the
+// serial band's code competes with it for the SM's instruction caches)
+template <int FM, bool CL, bool DIAG>
 __global__ void __launch_bounds__(256, 2) sc_decode_kernel(DecParams p)
 {
+    if (!DIAG) {
+        p.plain = 0;
+        p.dump = nullptr;
+        p.prof = nullptr;
+    }
     extern __shared__ __align__(16) unsigned char smem_raw[];
     __shared__ float red[32];
     const uint32_t S = p.S, N = p.N;
@@ -2108,14 +2116,16 @@ static int choose_K(const pq_decoder *h, int frames, int log2S, bool dump)
 template <int FM>
 static int launch_dec(const DecParams &p, int frames, int nthreads, size_t smem, cudaStream_t st)
 {
+    const bool diag = p.plain || p.dump || p.prof;
     if (p.K == 1) {
-        CUDA_TRY(cudaFuncSetAttribute(sc_decode_kernel<FM, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      (int)smem));
-        sc_decode_kernel<FM, false><<<frames, nthreads, smem, st>>>(p);
+        auto kern = diag ? sc_decode_kernel<FM, false, true> : sc_decode_kernel<FM, false, false>;
+        CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        kern<<<frames, nthreads, smem, st>>>(p);
         CUDA_TRY(cudaGetLastError());
         return 0;
     }
-    CUDA_TRY(cudaFuncSetAttribute(sc_decode_kernel<FM, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    auto ckern = diag ? sc_decode_kernel<FM, true, true> : sc_decode_kernel<FM, true, false>;
+    CUDA_TRY(cudaFuncSetAttribute(ckern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     cudaLaunchConfig_t cfg;
     memset(&cfg, 0, sizeof cfg);
     cfg.gridDim = dim3((unsigned)frames * p.K, 1, 1);
@@ -2129,7 +2139,7 @@ static int launch_dec(const DecParams &p, int frames, int nthreads, size_t smem,
     at[0].val.clusterDim.z = 1;
     cfg.attrs = at;
     cfg.numAttrs = 1;
-    CUDA_TRY(cudaLaunchKernelEx(&cfg, sc_decode_kernel<FM, true>, p));
+    CUDA_TRY(cudaLaunchKernelEx(&cfg, ckern, p));
     return 0;
 }
 
