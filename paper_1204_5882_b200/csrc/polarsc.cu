@@ -1713,24 +1713,38 @@ __global__ void __launch_bounds__(256, 2) sc_decode_kernel(DecParams p)
                 wsync(W > S);
                 const bool split = K > 1 && W > S;
                 const uint32_t lo = split ? slice_lo(W) : 0, hi = split ? lo + W / K : W;
+                // one pass: min |L| and, speculatively, the hard decisions (the
+                // node's own partial-sum words; a failed guard decodes the node
+                // normally, which rewrites them).  Each warp takes 256 elements
+                // (8 words) per iteration, all 8 loads in flight.
                 float m = __int_as_float(0x7f800000);
-                for (uint32_t i = lo + tid; i < hi; i += nthr) {
-                    const float v = d == 0 ? chan_load(p, fc, i) : src[i];
-                    m = fminf(m, fabsf(v));
+                uint32_t *xb = xptr(W);
+                const uint32_t base = xpos(W, j * W) >> 5;
+                {
+                    const int lane = tid & 31, wid = tid >> 5, nw = nthr >> 5;
+#pragma unroll 1
+                    for (uint32_t i0 = lo + 256u * wid; i0 < hi; i0 += 256u * nw) {
+                        float v[8];
+#pragma unroll
+                        for (int q = 0; q < 8; q++) {
+                            const uint32_t i = i0 + 32u * q + lane;
+                            v[q] = i < hi ? (d == 0 ? chan_load(p, fc, i) : src[i]) : __int_as_float(0x7f800000);
+                        }
+                        uint32_t word = 0;
+#pragma unroll
+                        for (int q = 0; q < 8; q++) {
+                            m = fminf(m, fabsf(v[q]));
+                            const uint32_t b = __ballot_sync(0xffffffffu, v[q] < 0.0f);
+                            if (lane == q) word = b;
+                        }
+                        if (lane < 8 && i0 + 32u * lane < hi) xb[base + ((i0 + 32u * lane) >> 5)] = word;
+                    }
                 }
                 m = block_min(m, red);
                 if (split) m = cluster_min(m, &cl_slot, K);
                 int k = 0;
                 for (uint32_t w = W; w > 1; w >>= 1) k++;
                 if (rate1_guard<FM>(m, k)) {
-                    uint32_t *xb = xptr(W);
-                    const uint32_t base = xpos(W, j * W) >> 5;
-                    for (uint32_t i0 = lo; i0 < hi; i0 += nthr) {
-                        const uint32_t i = i0 + tid;
-                        const float v = i < hi ? (d == 0 ? chan_load(p, fc, i) : src[i]) : 0.0f;
-                        const uint32_t bits = __ballot_sync(0xffffffffu, v < 0.0f);
-                        if ((tid & 31) == 0 && i < hi) xb[base + (i >> 5)] = bits;
-                    }
                     entering = false;
                     continue;
                 }
