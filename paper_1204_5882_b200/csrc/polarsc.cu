@@ -1273,6 +1273,110 @@ __device__ __noinline__ void warp_walk2(float *st_end, uint32_t *xs, const uint8
     UB_END(2);
 }
 
+// ---- the widest warp-band levels (W = 1024, 2048: SSC path): one warp takes
+// the node's f/g steps itself, from the shared-memory stage buffers (W/64 f's
+// per lane per step, independent), and hands the 512-wide children to
+// warp_walk2 -- no block barriers and no trip through the block-level main
+// loop for these nodes
+#ifndef PQ_WIDE_WARP_LOG2
+#define PQ_WIDE_WARP_LOG2 11
+#endif
+template <int FM, int W>
+__device__ __forceinline__ void warp_wide(float *st_end, uint32_t *xs, const uint8_t *ty, uint32_t S, int dS, int d0,
+                                          uint32_t j0)
+{
+    constexpr int V = W / 32, Vh = V / 2;
+    const unsigned FULL = 0xffffffffu;
+    const int lane = threadIdx.x & 31;
+    const int e = d0 - dS;
+    const uint32_t lh = (1u << e) + (j0 & ((1u << e) - 1u));
+    const float *nd = st_end - 2 * W;
+    float *ch = st_end - W;
+    uint32_t *xw = xs + (((j0 * W) & (S - 1)) >> 5);
+    const uint8_t t = ty[lh], tl = ty[2 * lh], tr = ty[2 * lh + 1];
+    if (t == NT_RATE0) {
+        for (int q = lane; q < V; q += 32) xw[q] = 0u;
+        __syncwarp();
+        return;
+    }
+    if (t == NT_RATE1) {
+        uint32_t m = 0x7f800000u;
+#pragma unroll 8
+        for (int q = 0; q < V; q++) m = min(m, __float_as_uint(nd[32 * q + lane]) & 0x7fffffffu);
+        m = __reduce_min_sync(FULL, m);
+        if (rate1_guard<FM>(__uint_as_float(m), ilog2((uint32_t)W))) {
+            for (int q = 0; q < V; q++) {
+                const uint32_t b = __ballot_sync(FULL, nd[32 * q + lane] < 0.0f);
+                if (lane == 0) xw[q] = b;
+            }
+            __syncwarp();
+            return;
+        }
+    }
+    if (t == NT_REP) {
+        // SC's g-chain with zero partial sums, in SC's pairing order
+        float acc[V];
+#pragma unroll
+        for (int q = 0; q < V; q++) acc[q] = nd[32 * q + lane];
+#pragma unroll
+        for (int hv = V / 2; hv >= 1; hv >>= 1)
+#pragma unroll
+            for (int q = 0; q < hv; q++) acc[q] = qadd<FM>(acc[q + hv], acc[q]);
+        float s0 = acc[0];
+#pragma unroll
+        for (int hh = 16; hh >= 1; hh >>= 1) s0 = qadd<FM>(__shfl_down_sync(FULL, s0, hh), s0);
+        const uint32_t bits = __shfl_sync(FULL, s0, 0) < 0.0f ? FULL : 0u;
+        for (int q = lane; q < V; q += 32) xw[q] = bits;
+        __syncwarp();
+        return;
+    }
+    // left child
+    if (tl == NT_RATE0) {
+        for (int q = lane; q < Vh; q += 32) xw[q] = 0u;
+        __syncwarp();
+    } else {
+#pragma unroll 8
+        for (int q = 0; q < Vh; q++) ch[32 * q + lane] = pq_f<FM>(nd[32 * q + lane], nd[32 * q + lane + W / 2]);
+        __syncwarp();
+        if constexpr (W / 2 > 512) warp_wide<FM, W / 2>(st_end, xs, ty, S, dS, d0 + 1, 2 * j0);
+        else warp_walk2<FM>(st_end, xs, ty, S, dS, d0 + 1, 2 * j0);
+    }
+    // right child: g-step with the left child's partial sums
+    if (tr == NT_RATE0) {
+        for (int q = lane; q < Vh; q += 32) xw[Vh + q] = 0u;
+        __syncwarp();
+    } else {
+#pragma unroll 8
+        for (int q = 0; q < Vh; q++)
+            ch[32 * q + lane] = pq_gt<FM>(nd[32 * q + lane], nd[32 * q + lane + W / 2], (xw[q] >> lane) & 1u);
+        __syncwarp();
+        if constexpr (W / 2 > 512) warp_wide<FM, W / 2>(st_end, xs, ty, S, dS, d0 + 1, 2 * j0 + 1);
+        else warp_walk2<FM>(st_end, xs, ty, S, dS, d0 + 1, 2 * j0 + 1);
+    }
+    for (int q = lane; q < Vh; q += 32) xw[q] ^= xw[Vh + q];
+    __syncwarp();
+}
+
+template <int FM>
+__device__ __noinline__ void warp_wide_root(float *st_end, uint32_t *xs, const uint8_t *ty, uint32_t S, int dS,
+                                            int d0, uint32_t j0)
+{
+    const uint32_t W = S >> (d0 - dS);
+#if PQ_WIDE_WARP_LOG2 >= 13
+    if (W == 8192) warp_wide<FM, 8192>(st_end, xs, ty, S, dS, d0, j0);
+    else
+#endif
+#if PQ_WIDE_WARP_LOG2 >= 12
+    if (W == 4096) warp_wide<FM, 4096>(st_end, xs, ty, S, dS, d0, j0);
+    else
+#endif
+#if PQ_WIDE_WARP_LOG2 >= 11
+    if (W == 2048) warp_wide<FM, 2048>(st_end, xs, ty, S, dS, d0, j0);
+    else
+#endif
+    warp_wide<FM, 1024>(st_end, xs, ty, S, dS, d0, j0);
+}
+
 template <int FM>
 __device__ __forceinline__ void warp_small(const float *src, bool chan, const DecParams &p, const FrameCtx &fc,
                                            uint32_t lh, const WarpCtx &wc, uint32_t *xs, uint32_t pos, int W)
@@ -1548,7 +1652,10 @@ __global__ void __launch_bounds__(256, 2) sc_decode_kernel(DecParams p)
     }
     __syncthreads();
     const int lw = lw_sh;
-    const uint32_t WMAX = S < p.wmax ? S : p.wmax;  // nodes this wide or narrower: one warp
+    // nodes this wide or narrower: one warp (the SSC path also takes the
+    // widest levels, 1024 / 2048, with warp_wide)
+    const uint32_t wmax_eff = (!p.plain && p.dump == nullptr && p.wmax == 512u) ? (1u << PQ_WIDE_WARP_LOG2) : p.wmax;
+    const uint32_t WMAX = S < wmax_eff ? S : wmax_eff;
 
     // TMA ring for the upper band (S >= 2048 so that chunks are >= 256 elements;
     // the stage dump keeps the register path)
@@ -1695,7 +1802,9 @@ __global__ void __launch_bounds__(256, 2) sc_decode_kernel(DecParams p)
 #ifndef PQ_WALK2
 #define PQ_WALK2 1
 #endif
-                        if (PQ_WALK2 && !p.plain && fc.dump == nullptr && W >= 64)
+                        if (!p.plain && fc.dump == nullptr && W > 512)
+                            warp_wide_root<FM>(sm.st + 2 * S, sm.xs, sm.ty, S, dS, d, j);
+                        else if (PQ_WALK2 && !p.plain && fc.dump == nullptr && W >= 64)
                             warp_walk2<FM>(sm.st + 2 * S, sm.xs, sm.ty, S, dS, d, j);
                         else
                             warp_walk<FM>(sm.st + 2 * S, sm.xs, sm.ty, fc.dump, N, S, dS, wc.jS, p.plain, d, j);
