@@ -624,3 +624,44 @@ def test_q88_input_matches_fp32_input(cuda):
         assert np.array_equal(from_words(u, N), ref)
     with pytest.raises(ValueError):
         ScDecoder(code, max_frames=F, f_mode="exact").decode_q88(torch.from_numpy(raw).to(cuda))
+
+
+# --------------------------------------------------------------------------
+# the widest warp-band levels (warp_wide: W = 1024, 2048 taken by one warp)
+
+def wide_node_code(n, rng):
+    """Blocks of 2048 / 1024 leaves that are rate-0, repetition, rate-1 or
+    mixed, so every node type reaches the 1024/2048 levels of the warp band."""
+    N = 1 << n
+    mask = np.zeros(N, np.uint8)
+    kinds = ["r0", "rep", "r1", "mix", "r1", "rep", "mix", "r0"]
+    for b in range(N // 1024):
+        blk = mask[1024 * b: 1024 * (b + 1)]
+        kind = kinds[b % len(kinds)]
+        if kind == "r0":
+            blk[:] = 1
+        elif kind == "rep":
+            blk[:-1] = 1
+        elif kind == "mix":
+            blk[:] = (rng.random(1024) < 0.5).astype(np.uint8)
+    return K.PolarCode(n=n, frozen_mask=mask, channel=C.BiAwgn(1.0), target_fer=0.1)
+
+
+@pytest.mark.parametrize("n,log2s", [(13, 0), (14, 11), (13, 12), (11, 0)])
+@pytest.mark.parametrize("strength", [1.0, 6.0])
+def test_warp_wide_levels_bit_exact(cuda, n, log2s, strength):
+    """Rate-1 guards that pass (strong LLRs) and fail (weak ones), repetition
+    sums and rate-0 children at widths 1024 / 2048, fp32 mirror and Q8.8."""
+    import torch
+    rng = np.random.default_rng(900 + n + log2s)
+    code = wide_node_code(n, rng)
+    F, N = 6, 1 << n
+    llr = (rng.normal(strength, 2.0, (F, N))).astype(np.float32)
+    fz = rng.integers(0, 2, (F, N)).astype(np.uint8)
+    ref, _ = oracle_batch(code, llr, fz, 32)
+    u, _ = gpu_decode(cuda, code, llr, fz, subtree_log2=log2s)
+    assert np.array_equal(u, ref)
+    raw = O.quantize_q88(llr)
+    dec = ScDecoder(code, max_frames=F, f_mode="fixed", subtree_log2=log2s)
+    u16, _ = dec.decode_q88(torch.from_numpy(raw).to(cuda), words_dev(fz, cuda))
+    assert np.array_equal(from_words(u16, N), fixed_oracle_batch(code, raw, fz))
