@@ -48,6 +48,7 @@ def parse():
     ap.add_argument("--no-ssc", action="store_true")
     ap.add_argument("--threads", type=int, default=0, choices=[0, 128, 256], help="threads per CTA (0 = auto)")
     ap.add_argument("--cluster", type=int, default=0, choices=[0, 1, 2, 4, 8], help="CTAs per frame (0 = auto)")
+    ap.add_argument("--subtree-log2", type=int, default=0, help="log2 of the shared-memory sub-tree width S (0 = auto)")
     ap.add_argument("--warp-log2", type=int, default=0, help="widest node of the single-warp band, log2 (0 = default)")
     ap.add_argument("--cpu-sample-s", type=float, default=10.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -271,7 +272,7 @@ def main():
     x_w = torch.from_numpy(pack_bits(x).view(np.int32).copy()).to(dev)
     u_w = polar_transform_words(x_w, n)  # Alice: u = T(x); the decoder reads u at frozen positions
     llr_d = torch.from_numpy(llr).to(dev)
-    dec = ScDecoder(code, max_frames=F, f_mode=args.fmode, ssc=not args.no_ssc)
+    dec = ScDecoder(code, max_frames=F, f_mode=args.fmode, ssc=not args.no_ssc, subtree_log2=args.subtree_log2)
     from paper_1204_5882_b200 import _lib
     if args.threads:
         dec.set_option(_lib.PQ_OPT_THREADS, args.threads)
