@@ -388,8 +388,19 @@ def main():
         err2 = int((last != u_w).any(dim=1).sum().item())
         assert err2 == errors, "e2e path decoded differently from the device path"
 
-    # statistics off the hot path (NCCL all-reduce of frame errors)
+    # statistics off the hot path (NCCL all-reduce of frame errors), and the
+    # decoded bits gathered over NVLink; both untimed
     stats = D.reduce_stats(torch.tensor([errors, F], dtype=torch.int64, device=dev))
+    gather = None
+    if world > 1:
+        g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        g0.record()
+        allu = D.gather_words(uh)
+        g1.record()
+        torch.cuda.synchronize()
+        assert allu.shape[0] == world * F
+        gather = {"collective": "all_gather (NCCL)", "bytes_per_rank": int(uh.numel() * 4),
+                  "ms": round(g0.elapsed_time(g1), 3)}
 
     if rank == 0:
         peaks = {}
@@ -418,7 +429,7 @@ def main():
                        "ctas_per_frame": launch_cfg["ctas_per_frame"],
                        "parallelism": f"frames sharded over {world} GPU(s)", "l2": "256 MiB flush between steps"},
             "fer": round(int(stats[0]) / int(stats[1]), 4), "frames_total": int(stats[1]),
-            "e2e": e2e, "gpu_launches": launches * args.steps,
+            "e2e": e2e, "gpu_launches": launches * args.steps, "gather_u_hat": gather,
             "roofline": with_traffic(roofline_entry(code, F, log2S, t_kernel, peaks, band_share, args.fmode), args),
             "kernel_ms": round(1e3 * t_kernel, 3),
             "cpu_baseline": cpu, "clocks": sampler.summary(), "wall_s_timed": round(t_wall, 3),
