@@ -46,7 +46,7 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--fmode", default="fixed", choices=["exact", "fast", "fixed", "min-sum"])
     ap.add_argument("--no-ssc", action="store_true")
-    ap.add_argument("--threads", type=int, default=0, choices=[0, 128, 256], help="threads per CTA (0 = auto)")
+    ap.add_argument("--threads", type=int, default=0, choices=[0, 64, 128, 256], help="threads per CTA (0 = auto)")
     ap.add_argument("--cluster", type=int, default=0, choices=[0, 1, 2, 4, 8], help="CTAs per frame (0 = auto)")
     ap.add_argument("--subtree-log2", type=int, default=0, help="log2 of the shared-memory sub-tree width S (0 = auto)")
     ap.add_argument("--warp-log2", type=int, default=0, help="widest node of the single-warp band, log2 (0 = default)")

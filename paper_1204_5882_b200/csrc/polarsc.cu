@@ -40,6 +40,7 @@
 #include <stdio.h>
 #include <stdlib.h>
 #include <string.h>
+#include <assert.h>
 
 #include <algorithm>
 #include <climits>
@@ -258,7 +259,12 @@ __device__ __forceinline__ float pq_g(float a, float b, uint32_t s) { return s ?
 // int/float conversions; the two lookups are independent).
 #define Q_MAX 32767.0f
 __constant__ float CORR_TAB_C[4097];
-__shared__ float pq_corrtab[4097];
+// C[k] = 0 for every k >= 1598 (256 ln(1 + e^(-k/256)) < 1/2), so the shared
+// copy keeps 2048 entries and f clamps its index at 2047 -- the same values as
+// the 4097-entry table clamped at 4096 (fixed_tables checks it), 8 KB less
+// shared memory per CTA
+#define CORR_SMEM 2048
+__shared__ float pq_corrtab[CORR_SMEM];
 
 template <int FM>
 __device__ __forceinline__ float qadd(float x, float y)
@@ -277,8 +283,8 @@ __device__ __forceinline__ int small_f2i(float x) { return __float_as_int(x + 12
 // magnitudes ma, mb (raw codes)
 __device__ __forceinline__ float pq_fmag_fixed(float ma, float mb)
 {
-    const int is = small_f2i(fminf(ma + mb, 4096.0f));
-    const int id = small_f2i(fminf(fabsf(ma - mb), 4096.0f));
+    const int is = small_f2i(fminf(ma + mb, (float)(CORR_SMEM - 1)));
+    const int id = small_f2i(fminf(fabsf(ma - mb), (float)(CORR_SMEM - 1)));
     return fmaxf(fminf(ma, mb) + pq_corrtab[is] - pq_corrtab[id], 0.0f);
 }
 
@@ -1623,7 +1629,7 @@ __global__ void __launch_bounds__(256, 2) sc_decode_kernel(DecParams p)
 
     load_log_table();
     if (FM == PQ_F_FIXED)
-        for (int i = threadIdx.x; i < 4097; i += blockDim.x) pq_corrtab[i] = CORR_TAB_C[i];
+        for (int i = threadIdx.x; i < CORR_SMEM; i += blockDim.x) pq_corrtab[i] = CORR_TAB_C[i];
     __syncthreads();
     const uint32_t K = CL ? p.K : 1u;  // CL = false: the single-CTA path compiles without slicing
     const uint32_t rank = blockIdx.x & (K - 1);  // CTA rank in the frame's cluster
@@ -1648,7 +1654,8 @@ __global__ void __launch_bounds__(256, 2) sc_decode_kernel(DecParams p)
     if (tid == 0) {
         uint32_t ws;
         asm volatile("mov.u32 %0, %%warpid;" : "=r"(ws));
-        lw_sh = (int)((ws / (uint32_t)(nthr >> 5)) & 3u);
+        const uint32_t nw = (uint32_t)(nthr >> 5);
+        lw_sh = (int)(((ws / nw) & 3u) % nw);
     }
     __syncthreads();
     const int lw = lw_sh;
@@ -2148,7 +2155,7 @@ __global__ void fmag_kernel(const float *a, const float *b, float *out, int n)
 {
     load_log_table();
     if (FM == PQ_F_FIXED)
-        for (int i = threadIdx.x; i < 4097; i += blockDim.x) pq_corrtab[i] = CORR_TAB_C[i];
+        for (int i = threadIdx.x; i < CORR_SMEM; i += blockDim.x) pq_corrtab[i] = CORR_TAB_C[i];
     __syncthreads();
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) out[i] = pq_f<FM>(a[i], b[i]);
 }
@@ -2272,6 +2279,8 @@ static int launch_dec(const DecParams &p, int frames, int nthreads, size_t smem,
 static int choose_threads(const pq_decoder *h, int frames)
 {
     if (h->threads_opt) return h->threads_opt;
+    // (64 -- 8 two-warp CTAs per SM, one wave for c2's 1024 frames -- measured
+    // 4 % slower than 128 on c2: the upper band loses more than the wave gains)
     return frames > 2 * h->sm_count ? 128 : 256;
 }
 
@@ -2283,14 +2292,14 @@ static int choose_log2S(const pq_decoder *h, int frames, int nthreads)
         return k < lo ? lo : k;
     }
     // resident CTAs per SM (the kernel's 128 registers per thread cap them)
-    const int cap = nthreads == 128 ? 4 : 2;
+    const int cap = nthreads == 64 ? 8 : nthreads == 128 ? 4 : 2;
     int per_sm = (frames + h->sm_count - 1) / h->sm_count;
     if (per_sm > cap) per_sm = cap;
     if (per_sm < 1) per_sm = 1;
     int best = 6;
     for (int k = 6; k <= 14; k++) {
         const size_t S = (size_t)1 << k;
-        const size_t bytes = 8 * S + (S / 32) * 4 + 2 * S + 18 * 1024;  // + static (table, barriers)
+        const size_t bytes = 8 * S + (S / 32) * 4 + 2 * S + 10 * 1024;  // + static (table, barriers)
         if ((size_t)per_sm * bytes <= 226 * 1024) best = k;
     }
     if (best > h->n) best = h->n;
@@ -2313,6 +2322,7 @@ static void fixed_tables(float *corr, float *tau)
         C[k] = (int)lrint(log1p(exp(-(double)k / 256.0)) * 256.0);
         corr[k] = (float)C[k];
     }
+    for (int k = CORR_SMEM - 1; k <= 4096; k++) assert(C[k] == 0);  // the shared copy's clamp is exact
     // L(a) = min over b >= a of |f(a, b)| = max(0, a + min_d (C[2a + d] - C[d]))
     // (d = b - a; both indices clamp at 4096, so d <= 4096 covers every b)
     std::vector<int> L(32768);
@@ -2478,7 +2488,8 @@ int pq_decoder_set_option(pq_decoder *h, int key, int value)
         h->warp_log2 = value;
         return 0;
     case PQ_OPT_THREADS:
-        if (value != 0 && value != 128 && value != 256) return set_err(-1, "threads must be 0 (auto), 128 or 256");
+        if (value != 0 && value != 64 && value != 128 && value != 256)
+            return set_err(-1, "threads must be 0 (auto), 64, 128 or 256");
         h->threads_opt = value;
         return 0;
     case PQ_OPT_CLUSTER:
