@@ -1610,8 +1610,10 @@ __device__ __forceinline__ float cluster_min(float m, float *slot, uint32_t K)
 // DIAG = false: the production instantiation -- no plain-SC mode, stage dump
 // or cycle profile in the code at all (a smaller, branch-free main loop: the
 // serial band's code competes with it for the SM's instruction caches)
-template <int FM, bool CL, bool DIAG>
-__global__ void __launch_bounds__(256, 2) sc_decode_kernel(DecParams p)
+// NT = 512: one CTA per SM (clusters with frames x K <= SMs, e.g. c5): twice
+// the warps for the upper band, whose per-CTA chunk work bounds it
+template <int FM, bool CL, bool DIAG, int NT>
+__global__ void __launch_bounds__(NT, NT == 512 ? 1 : 2) sc_decode_kernel(DecParams p)
 {
     if (!DIAG) {
         p.plain = 0;
@@ -2248,13 +2250,14 @@ static int launch_dec(const DecParams &p, int frames, int nthreads, size_t smem,
 {
     const bool diag = p.plain || p.dump || p.prof;
     if (p.K == 1) {
-        auto kern = diag ? sc_decode_kernel<FM, false, true> : sc_decode_kernel<FM, false, false>;
+        auto kern = diag ? sc_decode_kernel<FM, false, true, 256> : sc_decode_kernel<FM, false, false, 256>;
         CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         kern<<<frames, nthreads, smem, st>>>(p);
         CUDA_TRY(cudaGetLastError());
         return 0;
     }
-    auto ckern = diag ? sc_decode_kernel<FM, true, true> : sc_decode_kernel<FM, true, false>;
+    auto ckern = diag ? sc_decode_kernel<FM, true, true, 256>
+                      : nthreads == 512 ? sc_decode_kernel<FM, true, false, 512> : sc_decode_kernel<FM, true, false, 256>;
     CUDA_TRY(cudaFuncSetAttribute(ckern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     cudaLaunchConfig_t cfg;
     memset(&cfg, 0, sizeof cfg);
@@ -2601,7 +2604,7 @@ static int decode_impl(pq_decoder *h, const float *llr, const uint32_t *ybits, f
     DecParams p;
     memset(&p, 0, sizeof p);
     p.n = h->n;
-    const int nthreads = choose_threads(h, frames);
+    int nthreads = choose_threads(h, frames);
     p.log2S = choose_log2S(h, frames, nthreads);
     p.plain = (dump || !h->ssc) ? 1 : 0;
     p.frames = frames;
@@ -2626,6 +2629,13 @@ static int decode_impl(pq_decoder *h, const float *llr, const uint32_t *ybits, f
         p.mag = fminf(fmaxf(rintf(mag * 256.0f), -32767.0f), 32767.0f);
     }
     p.K = (uint32_t)choose_K(h, frames, p.log2S, dump != nullptr);
+#ifndef PQ_NT512
+#define PQ_NT512 1
+#endif
+    // clusters with one CTA per SM: 512 threads (production kernel only)
+    if (PQ_NT512 && h->threads_opt == 0 && p.K > 1 && !p.plain && !dump && !h->profile &&
+        (size_t)frames * p.K <= (size_t)h->sm_count)
+        nthreads = 512;
     h->last_K = (int)p.K;
     h->last_log2S = p.log2S;
     h->last_threads = nthreads;
