@@ -1539,7 +1539,9 @@ __device__ __forceinline__ float4 ring_val4(const DecParams &p, const UpSrc &u, 
 // dst: the output stage vector (global, or shared memory for a width-S
 // child).  All threads call it; thread 0 issues the copies.  ph holds the
 // CTA-uniform parity bit of every stage's mbarrier.
-template <int FM, bool IS_G>
+// SCR = true: both operands are fp32 stage vectors (no channel input, coset
+// or received-bit words) -- the common case, compiled without those branches
+template <int FM, bool IS_G, bool SCR>
 __device__ __forceinline__ void ring_step(const DecParams &p, const Ring &r, const UpSrc &u, float *dst, uint32_t lo,
                                           uint32_t hi, uint32_t &ph)
 {
@@ -1555,8 +1557,9 @@ __device__ __forceinline__ void ring_step(const DecParams &p, const Ring &r, con
         const uint32_t e0 = lo + c * C;
 #pragma unroll 1
         for (uint32_t k = 4 * tid; k < C; k += 4 * nthr) {
-            const float4 a = ring_val4<FM>(p, u, st, C, 0, k);
-            const float4 b = ring_val4<FM>(p, u, st, C, 1, k);
+            const float4 a = SCR ? *reinterpret_cast<const float4 *>(st + 4 * k) : ring_val4<FM>(p, u, st, C, 0, k);
+            const float4 b =
+                SCR ? *reinterpret_cast<const float4 *>(st + 4 * (size_t)C + 4 * k) : ring_val4<FM>(p, u, st, C, 1, k);
             float4 v;
             if (IS_G) {
                 const uint32_t *xw = reinterpret_cast<const uint32_t *>(st + 8 * C + 4 * (C / 8));
@@ -1918,7 +1921,8 @@ __global__ void __launch_bounds__(NT, NT == 512 ? 1 : 2) sc_decode_kernel(DecPar
                     u.a = src;
                     u.b = src + H;
                 }
-                ring_step<FM, false>(p, ring, u, dst, flo, fhi, ring_ph);
+                if (ch0) ring_step<FM, false, false>(p, ring, u, dst, flo, fhi, ring_ph);
+                else ring_step<FM, false, true>(p, ring, u, dst, flo, fhi, ring_ph);
             } else if (!ch0 && W > S && (fhi - flo) % (8 * nthr) == 0) {
                 // from HBM/L2: two chunks per thread in flight
 #pragma unroll 1
@@ -2035,7 +2039,8 @@ __global__ void __launch_bounds__(NT, NT == 512 ? 1 : 2) sc_decode_kernel(DecPar
                     u.b = src + W;
                 }
                 u.xl = fc.X + (j * W) / 32;  // the left child's bits (a width-S child's were copied out)
-                ring_step<FM, true>(p, ring, u, dst, glo, ghi, ring_ph);
+                if (ch0) ring_step<FM, true, false>(p, ring, u, dst, glo, ghi, ring_ph);
+                else ring_step<FM, true, true>(p, ring, u, dst, glo, ghi, ring_ph);
             }
             // g-step: W >= 256 here; 4 elements per thread, 4 chunks in flight
 #pragma unroll 1
