@@ -1948,18 +1948,32 @@ __global__ void __launch_bounds__(NT, NT == 512 ? 1 : 2) sc_decode_kernel(DecPar
                         *reinterpret_cast<float4 *>(dmp + i2) = v2;
                     }
                 }
-            } else
+            } else if (!ch0) {  // stage operands: no channel branches in the loop
 #pragma unroll 1
-            for (uint32_t i = flo + 4 * tid; i < fhi; i += 4 * nthr) {
-                const float4 a = ch0 ? chan_load4(p, fc, i) : *reinterpret_cast<const float4 *>(src + i);
-                const float4 b = ch0 ? chan_load4(p, fc, i + H) : *reinterpret_cast<const float4 *>(src + i + H);
-                float4 v;
-                v.x = pq_f<FM>(a.x, b.x);
-                v.y = pq_f<FM>(a.y, b.y);
-                v.z = pq_f<FM>(a.z, b.z);
-                v.w = pq_f<FM>(a.w, b.w);
-                *reinterpret_cast<float4 *>(dst + i) = v;
-                if (dmp) *reinterpret_cast<float4 *>(dmp + i) = v;
+                for (uint32_t i = flo + 4 * tid; i < fhi; i += 4 * nthr) {
+                    const float4 a = *reinterpret_cast<const float4 *>(src + i);
+                    const float4 b = *reinterpret_cast<const float4 *>(src + i + H);
+                    float4 v;
+                    v.x = pq_f<FM>(a.x, b.x);
+                    v.y = pq_f<FM>(a.y, b.y);
+                    v.z = pq_f<FM>(a.z, b.z);
+                    v.w = pq_f<FM>(a.w, b.w);
+                    *reinterpret_cast<float4 *>(dst + i) = v;
+                    if (dmp) *reinterpret_cast<float4 *>(dmp + i) = v;
+                }
+            } else {
+#pragma unroll 1
+                for (uint32_t i = flo + 4 * tid; i < fhi; i += 4 * nthr) {
+                    const float4 a = chan_load4(p, fc, i);
+                    const float4 b = chan_load4(p, fc, i + H);
+                    float4 v;
+                    v.x = pq_f<FM>(a.x, b.x);
+                    v.y = pq_f<FM>(a.y, b.y);
+                    v.z = pq_f<FM>(a.z, b.z);
+                    v.w = pq_f<FM>(a.w, b.w);
+                    *reinterpret_cast<float4 *>(dst + i) = v;
+                    if (dmp) *reinterpret_cast<float4 *>(dmp + i) = v;
+                }
             }
             d++;
             j = 2 * j;
@@ -2043,17 +2057,30 @@ __global__ void __launch_bounds__(NT, NT == 512 ? 1 : 2) sc_decode_kernel(DecPar
                 else ring_step<FM, true, true>(p, ring, u, dst, glo, ghi, ring_ph);
             }
             // g-step: W >= 256 here; 4 elements per thread, 4 chunks in flight
+            // (the operand loads are unswitched on the channel case)
 #pragma unroll 1
             for (uint32_t base = glo; base < (gring ? glo : ghi); base += 16 * nthr) {
                 float4 a[4], b[4];
                 uint32_t sb[4];
+                if (!ch0) {
 #pragma unroll
-                for (int k = 0; k < 4; k++) {
-                    const uint32_t i = base + 4 * (tid + k * nthr);
-                    if (i < ghi) {
-                        a[k] = ch0 ? chan_load4(p, fc, i) : *reinterpret_cast<const float4 *>(src + i);
-                        b[k] = ch0 ? chan_load4(p, fc, i + W) : *reinterpret_cast<const float4 *>(src + i + W);
-                        sb[k] = (xl[(lpos + i) >> 5] >> ((lpos + i) & 31)) & 15u;
+                    for (int k = 0; k < 4; k++) {
+                        const uint32_t i = base + 4 * (tid + k * nthr);
+                        if (i < ghi) {
+                            a[k] = *reinterpret_cast<const float4 *>(src + i);
+                            b[k] = *reinterpret_cast<const float4 *>(src + i + W);
+                            sb[k] = (xl[(lpos + i) >> 5] >> ((lpos + i) & 31)) & 15u;
+                        }
+                    }
+                } else {
+#pragma unroll
+                    for (int k = 0; k < 4; k++) {
+                        const uint32_t i = base + 4 * (tid + k * nthr);
+                        if (i < ghi) {
+                            a[k] = chan_load4(p, fc, i);
+                            b[k] = chan_load4(p, fc, i + W);
+                            sb[k] = (xl[(lpos + i) >> 5] >> ((lpos + i) & 31)) & 15u;
+                        }
                     }
                 }
 #pragma unroll
