@@ -181,6 +181,11 @@ def roofline_entry(code, frames, log2S, t_kernel_s, peaks, band_share=None, fmod
         up = alg / t_up / 1e9
         out["upper_band"] = {"time_share": round(band_share["upper"], 4), "achieved": round(up, 2),
                              "frac": round(up / peak, 4)}
+        if up > peak:
+            out["upper_band"]["note"] = (
+                "algorithmic bytes above the HBM peak: part of the stage traffic is served from L2 "
+                "(see traffic = ncu dram bytes per launch); the band is bound per CTA by its chunk work "
+                "(tools/upper_only.py, DESIGN.md section 7), not by HBM")
         out["band_share"] = {k: round(v, 4) for k, v in band_share.items()}
     return out
 
