@@ -66,7 +66,8 @@ extern "C" {
                                  0 = auto (more when frames < SMs), or 1, 2, 4, 8; it only
                                  applies when the block has an upper band and S >= 2048   */
 #define PQ_OPT_THREADS 7      /* threads per CTA: 0 = auto (256 up to 2 frames per SM, else
-                                 128 so that 4 frames share an SM), or 128 / 256            */
+                                 128 so that 4 frames share an SM; 512 when a clustered
+                                 batch leaves one CTA per SM), or 64 / 128 / 256          */
 
 /* slots of the per-frame profile record (pq_decoder_read_profile) */
 #define PQ_PROF_SLOTS 16
