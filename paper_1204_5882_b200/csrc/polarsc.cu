@@ -1439,6 +1439,16 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t by
                  : "memory");
 }
 
+// the same copy with an L2 evict-first policy: operands read for the last time
+__device__ __forceinline__ void bulk_g2s_ef(void *dst, const void *src, uint32_t bytes, uint64_t *bar)
+{
+    asm volatile("{\n\t.reg .b64 pol;\n\t"
+                 "createpolicy.fractional.L2::evict_first.b64 pol, 1.0;\n\t"
+                 "cp.async.bulk.shared::cta.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], pol;\n}"
+                 ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+
 __device__ __forceinline__ void fence_proxy_async()
 {
     asm volatile("fence.proxy.async;" ::: "memory");
@@ -1465,7 +1475,16 @@ struct Ring {
 };
 
 // stage layout: [A: C floats][B: C floats][ya][yb][ca][cb][xl] (C/32 words each)
-__device__ __forceinline__ void ring_issue(const Ring &r, const UpSrc &u, uint32_t e0, uint32_t s)
+#ifndef PQ_F_EF_BYTES
+#define PQ_F_EF_BYTES 0
+#endif
+#ifndef PQ_G_EVICT_FIRST
+#define PQ_G_EVICT_FIRST 1
+#endif
+// ef: the stage operands are read for the last time (a g-step reads its
+// parent node once, after the left sub-tree), so they are loaded evict-first
+// and leave L2 to the children the next steps re-read
+__device__ __forceinline__ void ring_issue(const Ring &r, const UpSrc &u, uint32_t e0, uint32_t s, bool ef = false)
 {
     unsigned char *st = reinterpret_cast<unsigned char *>(r.base) + (size_t)s * r.sbytes;
     const uint32_t C = r.C, wb = C / 8;  // bytes of C bits
@@ -1476,7 +1495,10 @@ __device__ __forceinline__ void ring_issue(const Ring &r, const UpSrc &u, uint32
     if (u.ca) bytes += 2 * wb;
     if (u.xl) bytes += wb;
     mbar_expect_tx(&r.bar[s], bytes);
-    if (u.a) {
+    if (u.a && ef) {
+        bulk_g2s_ef(st, u.a + e0, 4 * C, &r.bar[s]);
+        bulk_g2s_ef(st + 4 * C, u.b + e0, 4 * C, &r.bar[s]);
+    } else if (u.a) {
         bulk_g2s(st, u.a + e0, 4 * C, &r.bar[s]);
         bulk_g2s(st + 4 * C, u.b + e0, 4 * C, &r.bar[s]);
     }
@@ -1543,12 +1565,13 @@ __device__ __forceinline__ float4 ring_val4(const DecParams &p, const UpSrc &u, 
 // or received-bit words) -- the common case, compiled without those branches
 template <int FM, bool IS_G, bool SCR>
 __device__ __forceinline__ void ring_step(const DecParams &p, const Ring &r, const UpSrc &u, float *dst, uint32_t lo,
-                                          uint32_t hi, uint32_t &ph)
+                                          uint32_t hi, uint32_t &ph, bool ef_f = false)
 {
     const uint32_t C = r.C, D = r.D, tid = threadIdx.x, nthr = blockDim.x;
+    const bool ef = IS_G ? (bool)PQ_G_EVICT_FIRST : ef_f;
     const uint32_t nch = (hi - lo) / C;
     if (tid == 0)
-        for (uint32_t c = 0; c < nch && c < D; c++) ring_issue(r, u, lo + c * C, c);
+        for (uint32_t c = 0; c < nch && c < D; c++) ring_issue(r, u, lo + c * C, c, ef);
     uint32_t s = 0;
     for (uint32_t c = 0; c < nch; c++) {
         mbar_wait(&r.bar[s], (ph >> s) & 1u);
@@ -1577,7 +1600,7 @@ __device__ __forceinline__ void ring_step(const DecParams &p, const Ring &r, con
             *reinterpret_cast<float4 *>(dst + e0 + k) = v;
         }
         __syncthreads();  // stage s fully consumed
-        if (tid == 0 && c + D < nch) ring_issue(r, u, lo + (c + D) * C, s);
+        if (tid == 0 && c + D < nch) ring_issue(r, u, lo + (c + D) * C, s, ef);
         s = s + 1 == D ? 0 : s + 1;
     }
 }
@@ -1921,8 +1944,12 @@ __global__ void __launch_bounds__(NT, NT == 512 ? 1 : 2) sc_decode_kernel(DecPar
                     u.a = src;
                     u.b = src + H;
                 }
-                if (ch0) ring_step<FM, false, false>(p, ring, u, dst, flo, fhi, ring_ph);
-                else ring_step<FM, false, true>(p, ring, u, dst, flo, fhi, ring_ph);
+                // the parent's g-step re-read comes after its whole left
+                // sub-tree: when the level's parents outgrow L2 it cannot
+                // hit, so the f-step reads them evict-first as well
+                const bool f_ef = PQ_F_EF_BYTES > 0 && (uint64_t)8 * H * (gridDim.x / K) > (uint64_t)PQ_F_EF_BYTES;
+                if (ch0) ring_step<FM, false, false>(p, ring, u, dst, flo, fhi, ring_ph, f_ef);
+                else ring_step<FM, false, true>(p, ring, u, dst, flo, fhi, ring_ph, f_ef);
             } else if (!ch0 && W > S && (fhi - flo) % (8 * nthr) == 0) {
                 // from HBM/L2: two chunks per thread in flight
 #pragma unroll 1
