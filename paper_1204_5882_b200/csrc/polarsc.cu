@@ -1475,6 +1475,9 @@ struct Ring {
 };
 
 // stage layout: [A: C floats][B: C floats][ya][yb][ca][cb][xl] (C/32 words each)
+#ifndef PQ_ST_EVICT_LAST
+#define PQ_ST_EVICT_LAST 0
+#endif
 #ifndef PQ_F_EF_BYTES
 #define PQ_F_EF_BYTES 0
 #endif
@@ -1569,6 +1572,11 @@ __device__ __forceinline__ void ring_step(const DecParams &p, const Ring &r, con
 {
     const uint32_t C = r.C, D = r.D, tid = threadIdx.x, nthr = blockDim.x;
     const bool ef = IS_G ? (bool)PQ_G_EVICT_FIRST : ef_f;
+#if PQ_ST_EVICT_LAST
+    // children are re-read by the next step: keep them in L2
+    uint64_t st_pol;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(st_pol));
+#endif
     const uint32_t nch = (hi - lo) / C;
     if (tid == 0)
         for (uint32_t c = 0; c < nch && c < D; c++) ring_issue(r, u, lo + c * C, c, ef);
@@ -1597,7 +1605,13 @@ __device__ __forceinline__ void ring_step(const DecParams &p, const Ring &r, con
                 v.z = pq_f<FM>(a.z, b.z);
                 v.w = pq_f<FM>(a.w, b.w);
             }
+#if PQ_ST_EVICT_LAST
+            asm volatile("st.global.L2::cache_hint.v4.f32 [%0], {%1, %2, %3, %4}, %5;" ::"l"(dst + e0 + k), "f"(v.x),
+                         "f"(v.y), "f"(v.z), "f"(v.w), "l"(st_pol)
+                         : "memory");
+#else
             *reinterpret_cast<float4 *>(dst + e0 + k) = v;
+#endif
         }
         __syncthreads();  // stage s fully consumed
         if (tid == 0 && c + D < nch) ring_issue(r, u, lo + (c + D) * C, s, ef);
