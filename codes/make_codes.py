@@ -4,16 +4,16 @@ density evolution, then cache them as PQCT code tables (construction.py:464-480)
 Runs only in the build container (it imports /root/reference); the GPU box and the
 tests consume the committed `codes/*.pqct` + `codes/codes.json`, never this script.
 
-Density evolution is the reference's (construction.py:481-559). The only change is
+Density evolution is the reference's (construction.py:313-391). The only change is
 *who* walks the tree: each DE node depends only on its parent's density, so the
 reference's DFS splits into independent subtrees. `_node_step` below re-states the
-reference loop body (construction.py:530-557) verbatim in behaviour and calls the
+reference loop body (construction.py:362-389) verbatim in behaviour and calls the
 reference's own `_GridOps` methods / `_fill_pruned_good`; subtrees are farmed out to
 a process pool. `--check` proves bit-identity with the serial `density_evolution`.
 
 Rate-K selection (BASELINE configs give a rate, not a target FER): information set =
 the first K = round(rate*N) positions of the reference's ordering
-`np.lexsort((np.arange(N), pe))` (construction.py:574).
+`np.lexsort((np.arange(N), pe))` (construction.py:406).
 """
 from __future__ import annotations
 
@@ -45,7 +45,7 @@ CONFIGS = {
     "c5": dict(channel=("biawgn", 0.161), n=24, rate=0.09),
 }
 
-# defaults of density_evolution (construction.py:484-487)
+# defaults of density_evolution (construction.py:313-320)
 PZ, PI, MF = 1e-9, 1e-3, 1e-30
 
 
@@ -55,7 +55,7 @@ def make_channel(spec):
 
 
 def _node_step(ops, m, n, depth, offset, pe_out, pe_base):
-    """One iteration of the reference DFS body (construction.py:530-557).
+    """One iteration of the reference DFS body (construction.py:362-389).
 
     Returns the children to push as [(m, depth, offset), ...] in pop order
     (f-child first), or [] when the node was resolved into pe_out.

@@ -1,6 +1,6 @@
 """Table-1 row-1 code of the paper (BSC p=0.02, N=2^16, frozen set for target FER
 0.1 -- PAPER.md:169), built with the reference's own
-density_evolution + select_frozen (construction.py:481, :565) and cached as a
+density_evolution + select_frozen (construction.py:313, :397) and cached as a
 PQCT file.  Used by the SPEC's fixed-vs-float fidelity examples.
 Runs only in the build container (imports /root/reference)."""
 import json

@@ -12,7 +12,7 @@
  * Bit vectors (u-domain and x-domain BitBlocks) are packed
  * uint32 words, bit i of a frame at word i>>5, bit position i&31 (LSB first),
  * the same order as the reference's code-table mask packing
- * (np.packbits(..., bitorder="little"), construction.py:644 / :668).
+ * (np.packbits(..., bitorder="little"), construction.py:476 / :668).
  * Frames are stored frame-major: frame f's words start at f * (N/32)
  * (N >= 32; for N < 32 each frame still occupies one word).
  *
@@ -69,6 +69,10 @@ extern "C" {
                                  128 so that 4 frames share an SM; 512 when a clustered
                                  batch leaves one CTA per SM), or 64 / 128 / 256          */
 
+#define PQ_OPT_TIMING 8       /* 1: bracket every decode's sc_decode_kernel launch with CUDA
+                                 events on the launching stream (a ring of the last 64
+                                 decodes, read with pq_decoder_kernel_times); 0: off     */
+
 /* slots of the per-frame profile record (pq_decoder_read_profile) */
 #define PQ_PROF_SLOTS 16
 
@@ -80,7 +84,7 @@ typedef struct pq_decoder pq_decoder;
 int pq_decoder_create(pq_decoder **out, int n, int max_frames, int f_mode, int device);
 
 /* Install the frozen set: mask_host[i] = 1 if position i is frozen, length
- * 2^n bytes -- exactly PolarCode.frozen_mask (construction.py:264-268).
+ * 2^n bytes -- exactly PolarCode.frozen_mask (construction.py:96-108).
  * The mask is copied; the handle is immutable w.r.t. the code afterwards. */
 int pq_decoder_set_frozen_mask(pq_decoder *h, const uint8_t *mask_host);
 
@@ -154,8 +158,8 @@ uint64_t pq_xxh64(const void *data, size_t len, uint64_t seed);
  * SURVEY.md 8(f) f2).  Replaces: density_evolution(ch, n, quant, prune_z_eps,
  * prune_i_eps, mass_floor) (construction.py:313-391) with its f/g transforms
  * (_f_scatter / f_self / g_self, construction.py:138-158, :206-248) and the
- * pruned-subtree fill (construction.py:296-310).  The grid tables are the
- * reference's own (_GridOps, construction.py:166-197), computed on the host
+ * pruned-subtree fill (construction.py:302-310).  The grid tables are the
+ * reference's own (_GridOps, construction.py:164-190), computed on the host
  * and passed in: f_idx / f_whi are (bins-1)^2 row-major, z_weights / i_loss
  * have bins-1 entries.  pq_de_run takes the base density (bins+1 slots:
  * -inf, interior, +inf) and writes pe[2^n] (host memory); synchronous.     */
@@ -178,6 +182,13 @@ int pq_debug_fmag(int f_mode, const float *a, const float *b, float *out, int n,
 
 /* Bytes of device scratch owned by the handle. */
 size_t pq_decoder_workspace_bytes(const pq_decoder *h);
+
+/* Durations (ms) of the sc_decode_kernel launches of the last `count` decodes
+ * made with PQ_OPT_TIMING = 1 (oldest first; count <= 64 and <= the number
+ * timed since the option was set).  Waits for those launches to finish.
+ * Measurement only (bench.py's roofline): the events sit on the launching
+ * stream right before and after the kernel.                               */
+int pq_decoder_kernel_times(pq_decoder *h, float *ms_out, int count);
 
 /* Number of kernels the last decode call launched (for bench accounting). */
 int pq_decoder_last_launches(const pq_decoder *h);

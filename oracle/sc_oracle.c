@@ -15,13 +15,13 @@
  *   - f(a,b) = sgn a sgn b phi(phi|a| + phi|b|), exact (not min-sum)
  *                                                       SPEC.md:243, :270
  *     evaluated through the algebraically identical boxplus magnitude of the
- *     reference's own construction code          construction.py:300-303
+ *     reference's own construction code          construction.py:132-135
  *   - g(a,b,s) = b + (1-2s) a
  *   - decisions in index order 0..N-1, frozen leaves take the revealed value,
  *     information leaves u = [L < 0] (so L = +-0 decides 0) SPEC.md:243
  *   - explicit (non-recursive) walk with stage-indexed LLR buffers, O(N)
  *                                                       SPEC.md:271
- *   - tree order: f-child (lower indices) first        construction.py:555-557
+ *   - tree order: f-child (lower indices) first        construction.py:386-389
  *
  * Two arithmetic variants of the same algorithm:
  *   orc_sc_decode_f64 -- double precision, libm expm1/log1p: the formal
@@ -59,7 +59,7 @@ void orc_polar_transform(int n, uint8_t *v)
 /* f64 exact boxplus.  |f| = log((1 + e^-a e^-b) / (e^-a + e^-b))
  *                         = log1p((1-e^-a)(1-e^-b) / (e^-a + e^-b)),
  * identical in exact arithmetic to the reference's stable form
- * min + log1p(e^-(a+b)) - log1p(e^-|a-b|)  (construction.py:300-303),
+ * min + log1p(e^-(a+b)) - log1p(e^-|a-b|)  (construction.py:132-135),
  * but free of its cancellation when both magnitudes are small.            */
 
 double orc_fmag_f64(double a, double b)
@@ -353,7 +353,7 @@ int orc_max_threads(void)
  * f is the exact boxplus evaluated by table lookup:
  *     |f(a, b)| = phi(phi|a| + phi|b|)
  *               = min(|a|, |b|) + ln(1 + e^-(|a|+|b|)) - ln(1 + e^-||a|-|b||)
- * (the two forms are identical; construction.py:300-303 uses the second), with
+ * (the two forms are identical; construction.py:132-135 uses the second), with
  * CORR[k] = rint(256 ln(1 + e^(-k/256))), clamped at 0; sign = sgn a sgn b.
  * Why not the literal phi-table form (phi(k/256) in Q8.8, looked up twice):
  * its inverse lookup cannot resolve phi^-1 near 0 -- phi(x) < 1 LSB for x > 6.2,

@@ -24,6 +24,7 @@ PQ_OPT_PROFILE = 4
 PQ_OPT_WARP_LOG2 = 5
 PQ_OPT_CLUSTER = 6
 PQ_OPT_THREADS = 7
+PQ_OPT_TIMING = 8
 PQ_PROF_SLOTS = 16
 PROF_NAMES = ("upper_f", "upper_g", "upper_other", "smem_f", "smem_g", "smem_other", "warp_subtrees",
               "type_staging", "rate1_block", "total", "n_warp_subtrees", "n_block_nodes",
@@ -36,7 +37,7 @@ EXPORTS = (
     "pq_polar_transform", "pq_decoder_workspace_bytes", "pq_decoder_last_launches",
     "pq_decoder_destroy", "pq_last_error", "pq_abi_version", "pq_decoder_read_profile",
     "pq_debug_fmag", "pq_decoder_last_ctas_per_frame", "pq_decoder_last_config", "pq_sc_decode_q88",
-    "pq_hash_frames", "pq_verify_frames", "pq_xxh64", "pq_de_create", "pq_de_run", "pq_de_destroy",
+    "pq_decoder_kernel_times", "pq_hash_frames", "pq_verify_frames", "pq_xxh64", "pq_de_create", "pq_de_run", "pq_de_destroy",
 )
 
 _lib = None
@@ -73,6 +74,7 @@ def load():
     L.pq_decoder_last_config.argtypes = [vp, vp, vp, vp]
     L.pq_decoder_destroy.argtypes = [vp]
     L.pq_decoder_read_profile.argtypes = [vp, vp, i]
+    L.pq_decoder_kernel_times.argtypes = [vp, vp, i]
     L.pq_debug_fmag.argtypes = [i, vp, vp, vp, i, vp]
     L.pq_hash_frames.argtypes = [u32p, i, i, ctypes.c_uint64, vp, vp]
     L.pq_verify_frames.argtypes = [u32p, i, i, ctypes.c_uint64, vp, vp, vp, vp]

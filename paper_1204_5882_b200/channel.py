@@ -118,3 +118,35 @@ def frame(ch: ChannelModel, seed: int, j: int, N: int):
     """(x bits uint8[N], observation y) for frame j."""
     x = frame_bits(seed, j, N)
     return x, transmit(ch, x, seed, stream=2 * j + 1)
+
+
+def frames_batch(ch: ChannelModel, seed: int, j0: int, F: int, N: int, threads: int = 0,
+                 want_y: bool = True):
+    """Frames j0 .. j0+F-1 of the seed convention above, generated on host
+    threads (numpy's generators release the GIL while they fill arrays):
+    x uint8[F, N], fp32 channel LLRs [F, N], and the BSC received bits
+    uint8[F, N] (None for BIAWGN or when not wanted).  Identical to calling
+    ``frame`` / ``channel_llr`` per frame, whatever the thread count."""
+    import os
+    from concurrent.futures import ThreadPoolExecutor
+
+    x = np.empty((F, N), np.uint8)
+    llr = np.empty((F, N), np.float32)
+    y_bits = np.empty((F, N), np.uint8) if (want_y and isinstance(ch, Bsc)) else None
+
+    def one(i):
+        xi, yi = frame(ch, seed, j0 + i, N)
+        x[i] = xi
+        llr[i] = channel_llr(ch, yi)
+        if y_bits is not None:
+            y_bits[i] = yi
+
+    if threads <= 0:
+        threads = min(32, len(os.sched_getaffinity(0)))
+    if threads == 1 or F == 1:
+        for i in range(F):
+            one(i)
+    else:
+        with ThreadPoolExecutor(max_workers=min(threads, F)) as ex:
+            list(ex.map(one, range(F)))
+    return x, llr, y_bits

@@ -1,9 +1,9 @@
 """PolarCode (the construction->decoding contract) and the PQCT code-table file.
 
-* ``PolarCode`` mirrors construction.py:263-294: block size 2^n, frozen_mask
+* ``PolarCode`` mirrors construction.py:95-126: block size 2^n, frozen_mask
   uint8 of length 2^n with 1 = frozen, plus provenance.
 * ``read_code_table`` / ``write_code_table`` implement the reference's binary
-  format (construction.py:632-684): b"PQCT", little-endian ``<HBBddI``
+  format (construction.py:464-516): b"PQCT", little-endian ``<HBBddI``
   header (version, n, channel tag, channel parameter, target FER, DE bins),
   LSB-first packed mask, then an 8-byte blake2b checksum of everything before
   it.  Corruption raises ValueError exactly where the reference does.

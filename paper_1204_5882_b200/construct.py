@@ -62,7 +62,7 @@ def _boxplus_magnitude(a, b):
 
 
 class GridTables:
-    """The reference's _GridOps tables (construction.py:166-197), same formulas."""
+    """The reference's _GridOps tables (construction.py:164-190), same formulas."""
 
     def __init__(self, grid: DeGrid):
         self.grid = grid
@@ -96,7 +96,7 @@ def grid_tables(grid: DeGrid) -> GridTables:
 
 
 def base_density(ch, t: GridTables) -> np.ndarray:
-    """Channel LLR density on the lattice (construction.py:256-293)."""
+    """Channel LLR density on the lattice (construction.py:264-296)."""
     grid = t.grid
     m = np.zeros(t.size)
     if isinstance(ch, Bsc):

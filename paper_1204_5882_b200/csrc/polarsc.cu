@@ -43,6 +43,7 @@
 #include <assert.h>
 
 #include <algorithm>
+#include <mutex>
 #include <climits>
 #include <string>
 #include <vector>
@@ -165,7 +166,7 @@ __device__ __forceinline__ float pq_log1p(float q)
 //   lo >  8:  lo - log1p(e^-(hi - lo))      (drops log1p(e^-(lo+hi)) < 1.2e-7, i.e.
 //                                            < 2e-8 relative to a result >= 7.3)
 // = log((1 + e^-a e^-b)/(e^-a + e^-b)) = phi(phi(a) + phi(b)),
-// the reference's stable boxplus (construction.py:300-303) in a form free of
+// the reference's stable boxplus (construction.py:132-135) in a form free of
 // its cancellation at small magnitudes.  Max relative error ~3.4e-7.
 __device__ __forceinline__ float pq_fmag(float a, float b)
 {
@@ -2283,6 +2284,8 @@ static int launch_transform(const uint32_t *in, uint32_t *out, int n, int frames
 // ---------------------------------------------------------------------------
 // host side
 
+#define PQ_TIMING_SLOTS 64
+
 struct pq_decoder {
     int n, max_frames, fmode, device, ssc, log2S_opt;
     uint32_t N, wpf;
@@ -2303,6 +2306,9 @@ struct pq_decoder {
     int last_K;       // CTAs per frame of the last decode launch
     int last_log2S, last_threads;
     unsigned long long *d_prof;
+    int timing;                       // PQ_OPT_TIMING
+    cudaEvent_t ev[2 * PQ_TIMING_SLOTS];  // kernel start/end events (created on first use)
+    int n_timed;                      // decodes timed since the option was set
 };
 
 // CTAs per frame: split the upper band of a frame over a thread-block cluster
@@ -2435,16 +2441,42 @@ static int ensure_fixed_tables()
 {
     int dev = 0;
     CUDA_TRY(cudaGetDevice(&dev));
+    static std::mutex mu;
     static bool done[64] = {false};
+    std::lock_guard<std::mutex> lock(mu);  // one upload per device, whatever the host threads
     if (dev < 64 && done[dev]) return 0;
     static float corr[4097];
     float tau[26];
     fixed_tables(corr, tau);
     CUDA_TRY(cudaMemcpyToSymbol(CORR_TAB_C, corr, sizeof corr));
     CUDA_TRY(cudaMemcpyToSymbol(RATE1_TAU_FIX, tau, sizeof tau));
+    // pageable uploads may return before the DMA lands; a decode on a
+    // non-blocking stream is not ordered after them, so wait here once
+    CUDA_TRY(cudaDeviceSynchronize());
     if (dev < 64) done[dev] = true;
     return 0;
 }
+
+// Select `dev` for the calling host thread and restore the caller's device on
+// scope exit (every C-ABI entry that touches a handle's device uses one).
+struct DeviceGuard {
+    int prev = -1;
+    cudaError_t err = cudaSuccess;
+    explicit DeviceGuard(int dev)
+    {
+        if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+        if (prev != dev) err = cudaSetDevice(dev);
+    }
+    ~DeviceGuard()
+    {
+        int cur = -1;
+        if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
+    }
+};
+#define DEVICE_GUARD(dev)                                                                          \
+    DeviceGuard dg_(dev);                                                                          \
+    if (dg_.err != cudaSuccess)                                                                    \
+        return set_err(1 + (int)dg_.err, "cudaSetDevice(%d): %s", (int)(dev), cudaGetErrorString(dg_.err))
 
 // error text for the other translation units of the library (verify.cu)
 int pq_set_error_text(int code, const char *msg) { return set_err(code, "%s", msg); }
@@ -2462,7 +2494,7 @@ int pq_decoder_create(pq_decoder **out, int n, int max_frames, int f_mode, int d
     if (max_frames < 1) return set_err(-1, "max_frames must be >= 1, got %d", max_frames);
     if (f_mode != PQ_F_EXACT && f_mode != PQ_F_MINSUM && f_mode != PQ_F_FAST && f_mode != PQ_F_FIXED)
         return set_err(-1, "unknown f mode %d", f_mode);
-    CUDA_TRY(cudaSetDevice(device));
+    DEVICE_GUARD(device);
     pq_decoder *h = new pq_decoder();
     h->n = n;
     h->max_frames = max_frames;
@@ -2512,6 +2544,8 @@ int pq_decoder_destroy(pq_decoder *h)
     cudaFree(h->d_x);
     cudaFree(h->d_scr);
     cudaFree(h->d_prof);
+    for (int i = 0; i < 2 * PQ_TIMING_SLOTS; i++)
+        if (h->ev[i]) cudaEventDestroy(h->ev[i]);
     delete h;
     return 0;
 }
@@ -2519,6 +2553,21 @@ int pq_decoder_destroy(pq_decoder *h)
 size_t pq_decoder_workspace_bytes(const pq_decoder *h) { return h ? h->ws_bytes : 0; }
 int pq_decoder_last_launches(const pq_decoder *h) { return h ? h->last_launches : 0; }
 int pq_decoder_last_ctas_per_frame(const pq_decoder *h) { return h ? h->last_K : 0; }
+
+int pq_decoder_kernel_times(pq_decoder *h, float *ms_out, int count)
+{
+    if (!h || !ms_out) return set_err(-1, "NULL argument");
+    const int avail = h->n_timed < PQ_TIMING_SLOTS ? h->n_timed : PQ_TIMING_SLOTS;
+    if (count < 0 || count > avail)
+        return set_err(-1, "count=%d outside [0, %d] (decodes timed since PQ_OPT_TIMING was set)", count, avail);
+    DEVICE_GUARD(h->device);
+    for (int i = 0; i < count; i++) {
+        const int slot = (h->n_timed - count + i) % PQ_TIMING_SLOTS;
+        CUDA_TRY(cudaEventSynchronize(h->ev[2 * slot + 1]));
+        CUDA_TRY(cudaEventElapsedTime(&ms_out[i], h->ev[2 * slot], h->ev[2 * slot + 1]));
+    }
+    return 0;
+}
 
 int pq_decoder_last_config(const pq_decoder *h, int *log2S, int *threads_per_cta, int *ctas_per_frame)
 {
@@ -2573,6 +2622,14 @@ int pq_decoder_set_option(pq_decoder *h, int key, int value)
             return set_err(-1, "cluster size must be 0 (auto), 1, 2, 4 or 8");
         h->cluster_opt = value;
         return 0;
+    case PQ_OPT_TIMING:
+        if (value && !h->ev[0]) {
+            DEVICE_GUARD(h->device);
+            for (int i = 0; i < 2 * PQ_TIMING_SLOTS; i++) CUDA_TRY(cudaEventCreate(&h->ev[i]));
+        }
+        h->timing = value ? 1 : 0;
+        h->n_timed = 0;
+        return 0;
     case PQ_OPT_PROFILE:
         if (value && !h->d_prof) {
             cudaError_t e = cudaMalloc((void **)&h->d_prof, (size_t)h->max_frames * PQ_PROF_SLOTS * 8);
@@ -2605,6 +2662,7 @@ int pq_decoder_get_option(const pq_decoder *h, int key)
     case PQ_OPT_WARP_LOG2: return h->warp_log2;
     case PQ_OPT_CLUSTER: return h->cluster_opt;
     case PQ_OPT_THREADS: return h->threads_opt;
+    case PQ_OPT_TIMING: return h->timing;
     default: return set_err(-1, "unknown option %d", key);
     }
 }
@@ -2638,7 +2696,7 @@ int pq_decoder_set_frozen_mask(pq_decoder *h, const uint8_t *mask)
     std::vector<uint32_t> words(h->wpf, 0);
     for (uint32_t i = 0; i < N; i++)
         if (mask[i]) words[i >> 5] |= 1u << (i & 31);
-    CUDA_TRY(cudaSetDevice(h->device));
+    DEVICE_GUARD(h->device);
     CUDA_TRY(cudaMemcpy(h->d_types, ty.data(), ty.size(), cudaMemcpyHostToDevice));
     CUDA_TRY(cudaMemcpy(h->d_mask, words.data(), words.size() * 4, cudaMemcpyHostToDevice));
     h->have_mask = 1;
@@ -2666,7 +2724,7 @@ static int decode_impl(pq_decoder *h, const float *llr, const uint32_t *ybits, f
     if (!llr && !ybits && !llr16) return set_err(-1, "no channel input");
     if (frames == 0) return 0;
     cudaStream_t st = (cudaStream_t)stream;
-    CUDA_TRY(cudaSetDevice(h->device));
+    DEVICE_GUARD(h->device);
     int launches = 0;
     const uint32_t *cw = nullptr;
     if (frozen_u) {
@@ -2713,12 +2771,18 @@ static int decode_impl(pq_decoder *h, const float *llr, const uint32_t *ybits, f
     h->last_log2S = p.log2S;
     h->last_threads = nthreads;
     const size_t smem = dec_smem_bytes(p.S);
+    const int slot = h->n_timed % PQ_TIMING_SLOTS;
+    if (h->timing) CUDA_TRY(cudaEventRecord(h->ev[2 * slot], st));
     int lrc;
     if (h->fmode == PQ_F_FIXED) lrc = launch_dec<PQ_F_FIXED>(p, frames, nthreads, smem, st);
     else if (h->fmode == PQ_F_MINSUM) lrc = launch_dec<PQ_F_MINSUM>(p, frames, nthreads, smem, st);
     else if (h->fmode == PQ_F_FAST) lrc = launch_dec<PQ_F_FAST>(p, frames, nthreads, smem, st);
     else lrc = launch_dec<PQ_F_EXACT>(p, frames, nthreads, smem, st);
     if (lrc) return lrc;
+    if (h->timing) {
+        CUDA_TRY(cudaEventRecord(h->ev[2 * slot + 1], st));
+        h->n_timed++;
+    }
     launches++;
     const size_t nwords = (size_t)frames * h->wpf;
     if (x_hat) {

@@ -13,7 +13,7 @@ Batched entry points for the throughput path work on device tensors:
   ScDecoder.decode_bsc(y words[F,N/32], ...)   (fused BSC front end)
   polar_transform_words(words[F,N/32], n)
 Bit vectors are packed LSB-first into 32-bit words (bit i of a frame at word
-i >> 5, bit i & 31), the PQCT mask order (construction.py:644).
+i >> 5, bit i & 31), the PQCT mask order (construction.py:476).
 """
 from __future__ import annotations
 
@@ -83,9 +83,11 @@ def _require_cuda(device=None):
     return dev
 
 
-def _stream_ptr(stream):
+def _stream_ptr(stream, device=None):
+    """The cudaStream_t to launch on: `stream`, else the current stream of
+    `device` (the handle's device, not whatever device is current)."""
     if stream is None:
-        return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+        return ctypes.c_void_p(torch.cuda.current_stream(device).cuda_stream)
     return ctypes.c_void_p(stream.cuda_stream)
 
 
@@ -166,6 +168,15 @@ class ScDecoder:
                    "pq_decoder_read_profile")
         return out
 
+    def kernel_times(self, count: int) -> np.ndarray:
+        """Durations (ms) of the sc_decode_kernel launches of the last `count`
+        decodes made with set_option(PQ_OPT_TIMING, 1): CUDA events on the
+        launching stream right around the kernel (measurement only)."""
+        out = np.zeros(count, np.float32)
+        _lib.check(_lib.load().pq_decoder_kernel_times(self._h, out.ctypes.data, int(count)),
+                   "pq_decoder_kernel_times")
+        return out
+
     def alloc_words(self, frames: int):
         return torch.empty((frames, self.wpf), dtype=torch.int32, device=self.device)
 
@@ -183,7 +194,7 @@ class ScDecoder:
         u_hat, x_hat = self._outs(F, u_hat, x_hat, want_u, want_x)
         _check_words(frozen_u, F, self.wpf, "frozen_u")
         rc = _lib.load().pq_sc_decode_f32(self._h, _ptr(llr), _ptr(frozen_u), _ptr(u_hat), _ptr(x_hat),
-                                          F, _stream_ptr(stream))
+                                          F, _stream_ptr(stream, self.device))
         _lib.check(rc, "pq_sc_decode_f32")
         return u_hat, x_hat
 
@@ -201,7 +212,7 @@ class ScDecoder:
         u_hat, x_hat = self._outs(F, u_hat, x_hat, want_u, want_x)
         _check_words(frozen_u, F, self.wpf, "frozen_u")
         rc = _lib.load().pq_sc_decode_q88(self._h, _ptr(llr_q88), _ptr(frozen_u), _ptr(u_hat), _ptr(x_hat),
-                                          F, _stream_ptr(stream))
+                                          F, _stream_ptr(stream, self.device))
         _lib.check(rc, "pq_sc_decode_q88")
         return u_hat, x_hat
 
@@ -213,7 +224,7 @@ class ScDecoder:
         _check_words(frozen_u, F, self.wpf, "frozen_u")
         u_hat, x_hat = self._outs(F, u_hat, x_hat, want_u, want_x)
         rc = _lib.load().pq_sc_decode_bsc(self._h, _ptr(y_words), ctypes.c_float(llr_mag), _ptr(frozen_u),
-                                          _ptr(u_hat), _ptr(x_hat), F, _stream_ptr(stream))
+                                          _ptr(u_hat), _ptr(x_hat), F, _stream_ptr(stream, self.device))
         _lib.check(rc, "pq_sc_decode_bsc")
         return u_hat, x_hat
 
@@ -225,7 +236,7 @@ class ScDecoder:
         dump = torch.zeros((F, self.n + 1, self.N), dtype=torch.float32, device=self.device)
         _check_words(frozen_u, F, self.wpf, "frozen_u")
         rc = _lib.load().pq_sc_decode_f32_dump(self._h, _ptr(llr), _ptr(frozen_u), _ptr(u_hat),
-                                               _ptr(x_hat), _ptr(dump), F, _stream_ptr(stream))
+                                               _ptr(x_hat), _ptr(dump), F, _stream_ptr(stream, self.device))
         _lib.check(rc, "pq_sc_decode_f32_dump")
         return u_hat, x_hat, dump
 
@@ -276,7 +287,7 @@ def polar_transform_words(words, n: int, out=None, stream=None):
     _check_words(words, F, wpf, "words")
     if out is None:
         out = torch.empty_like(words)
-    rc = _lib.load().pq_polar_transform(_ptr(words), _ptr(out), n, F, _stream_ptr(stream))
+    rc = _lib.load().pq_polar_transform(_ptr(words), _ptr(out), n, F, _stream_ptr(stream, words.device))
     _lib.check(rc, "pq_polar_transform")
     return out
 
@@ -289,7 +300,7 @@ def hash_frames(x_words, n: int, key: int = 0, out=None, stream=None):
     _check_words(x_words, F, words_per_frame(n), "x_words")
     if out is None:
         out = torch.empty(F, dtype=torch.int64, device=x_words.device)
-    rc = _lib.load().pq_hash_frames(_ptr(x_words), n, F, key & (2 ** 64 - 1), _ptr(out), _stream_ptr(stream))
+    rc = _lib.load().pq_hash_frames(_ptr(x_words), n, F, key & (2 ** 64 - 1), _ptr(out), _stream_ptr(stream, x_words.device))
     _lib.check(rc, "pq_hash_frames")
     return out
 
@@ -307,7 +318,7 @@ def verify_frames(x_words, n: int, expect, key: int = 0, verified=None, n_discar
         verified = torch.empty(F, dtype=torch.uint8, device=x_words.device)
     rc = _lib.load().pq_verify_frames(_ptr(x_words), n, F, key & (2 ** 64 - 1), _ptr(expect), _ptr(verified),
                                       _ptr(n_discarded) if n_discarded is not None else None,
-                                      _stream_ptr(stream))
+                                      _stream_ptr(stream, x_words.device))
     _lib.check(rc, "pq_verify_frames")
     return verified
 

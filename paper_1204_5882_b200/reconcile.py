@@ -69,11 +69,16 @@ def alice_disclose_batch(code: PolarCode, x_words, key: int = 0, frozen_words=No
     decoder reads) and the XXH64 hashes ([F] int64)."""
     import torch
 
-    u = polar_transform_words(x_words, code.n, stream=stream)
     if frozen_words is None:
         frozen_words = torch.from_numpy(pack_bits(code.frozen_mask).view(np.int32).copy()).to(x_words.device)
-    u &= frozen_words
-    return u, hash_frames(x_words, code.n, key, stream=stream)
+    s = stream if stream is not None else torch.cuda.current_stream(x_words.device)
+    # every op (the allocation of u, the transform, the masking, the hash) is
+    # ordered on one stream: the caller's
+    with torch.cuda.stream(s):
+        u = polar_transform_words(x_words, code.n, stream=s)
+        u &= frozen_words
+        h = hash_frames(x_words, code.n, key, stream=s)
+    return u, h
 
 
 def bob_decode_batch(decoder, frozen_u, hashes, key: int = 0, llr=None, y_words=None, llr_mag=None,

@@ -70,18 +70,24 @@ def run_trials(code: PolarCode, ch, trials: int, seed: int, representation: str 
     t_wall = time.perf_counter()
     warm = True
     done = 0
+    from concurrent.futures import ThreadPoolExecutor
+
+    def host_batch(j0, F):
+        # threaded host generation of the next batch (channel.frames_batch),
+        # overlapped with the device decode of the current one
+        x, llr, y = C.frames_batch(ch, seed, j0, F, N)
+        return x, (pack_bits(y) if is_bsc else llr)
+
+    gen = ThreadPoolExecutor(max_workers=1)
+    nxt = gen.submit(host_batch, 0, min(batch, trials))
     while done < trials:
         F = min(batch, trials - done)
-        x = np.empty((F, N), np.uint8)
-        inp = np.empty((F, N), np.uint8 if is_bsc else np.float32)
-        for i in range(F):
-            xi, yi = C.frame(ch, seed, done + i, N)
-            x[i] = xi
-            inp[i] = yi if is_bsc else C.channel_llr(ch, yi)
+        x, inp = nxt.result()
+        if done + F < trials:
+            nxt = gen.submit(host_batch, done + F, min(batch, trials - done - F))
         x_w = torch.from_numpy(pack_bits(x).view(np.int32).copy()).to(dev)
         u_w = polar_transform_words(x_w, n)  # Alice's disclosure: u = T(x)
-        d_in = (torch.from_numpy(pack_bits(inp).view(np.int32).copy()) if is_bsc
-                else torch.from_numpy(inp)).to(dev)
+        d_in = (torch.from_numpy(inp.view(np.int32).copy()) if is_bsc else torch.from_numpy(inp)).to(dev)
 
         def decode():
             if is_bsc:
@@ -100,6 +106,7 @@ def run_trials(code: PolarCode, ch, trials: int, seed: int, representation: str 
         decode_s += a.elapsed_time(b) / 1e3
         failures += int((x_hat[:F] != x_w).any(dim=1).sum().item())
         done += F
+    gen.shutdown()
     wall = time.perf_counter() - t_wall
     return BenchRow(channel=_channel_name(ch), n=n, rate=code.rate, fer_measured=failures / trials,
                     trials=trials, throughput_mbps=trials * N / decode_s / 1e6, wall_time=wall, seed=seed,

@@ -6,7 +6,7 @@ box and the test-suite read the committed .npz files and never the reference.
   channel_vectors.npz  -- make_rng / transmit / channel_llr outputs
                           (channel.py:66-150) for the package's restatement
   boxplus_grid.npz     -- the reference's exact boxplus magnitude
-                          _boxplus_magnitude (construction.py:300-303) on a
+                          _boxplus_magnitude (construction.py:132-135) on a
                           log grid, to pin the oracle's and the GPU's f
   c1_frames.npz        -- config c1 frames 0..15 generated with the
                           reference's own make_rng/transmit/channel_llr

@@ -1,0 +1,163 @@
+"""Parity at the launch shapes bench.py times (VERDICT r01 "What's weak" #1).
+
+The decoder's launch shape depends on the frame count (choose_K, choose_threads,
+choose_log2S, the 512-thread rule in decode_impl), so the smaller batches of
+test_gpu_parity.py run different shapes from the benchmark.  These tests decode
+the FULL BASELINE batches with automatic options -- exactly the shapes the bench
+times -- and compare every frame's u-hat with the oracle:
+
+  c2: 1024 frames -> 128-thread CTAs, 4 per SM, S = 2^11
+  c3, c4: 256 frames -> one CTA per frame, 256 threads, S = 2^13, TMA ring
+  c5: 32 frames (N = 2^24) -> clusters of 4 CTAs, 512 threads, S = 2^14
+
+plus a determinism sweep over cluster size x threads per CTA x sub-tree width
+(identical outputs across runs and thread counts).
+Fixed point is compared with the integer oracle, exact mode with the fp32
+mirror, both bit for bit on every frame.
+"""
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+from paper_1204_5882_b200 import _lib
+from paper_1204_5882_b200 import channel as C
+from paper_1204_5882_b200 import codes as K
+from paper_1204_5882_b200.polar_core import ScDecoder, pack_bits, unpack_bits
+
+pytestmark = pytest.mark.gpu
+
+# (frames, expected launch shape: subtree_log2, threads_per_cta, ctas_per_frame) on a 148-SM B200
+BENCH_SHAPES = {
+    "c2": (1024, (11, 128, 1)),
+    "c3": (256, (13, 256, 1)),
+    "c4": (256, (13, 256, 1)),
+    "c5": (32, (14, 512, 4)),
+}
+
+_batches = {}
+
+
+def batch(key, frames):
+    """Frames 0..frames-1 of config `key` (bench.py's frames) with u = T(x)."""
+    if (key, frames) not in _batches:
+        cfg = K.CONFIGS[key]
+        code = K.load_config(key)
+        x, llr, _ = C.frames_batch(cfg.channel, cfg.seed, 0, frames, code.block_size, want_y=False)
+        u = np.empty_like(x)
+        for f in range(frames):
+            u[f] = O.polar_transform_bytes(x[f])
+        _batches.clear()
+        _batches[(key, frames)] = (code, x, u, llr)
+    return _batches[(key, frames)]
+
+
+def dev_words(bits, dev):
+    import torch
+    return torch.from_numpy(pack_bits(bits).view(np.int32).copy()).to(dev)
+
+
+def oracle(code, llr, u, fmode):
+    prec = 16 if fmode == "fixed" else 32
+    return O.sc_decode_batch(code.frozen_mask, llr, u, precision=prec, threads=O.max_threads())
+
+
+def sm_count():
+    import torch
+    return torch.cuda.get_device_properties(0).multi_processor_count
+
+
+@pytest.mark.parametrize("fmode", ["fixed", "exact"])
+@pytest.mark.parametrize("key", list(BENCH_SHAPES))
+def test_bench_batch_matches_oracle(cuda, key, fmode):
+    import torch
+    if key not in K.available_configs():
+        pytest.skip(f"{key}.pqct not built")
+    frames, shape = BENCH_SHAPES[key]
+    code, x, u, llr = batch(key, frames)
+    N = code.block_size
+    dec = ScDecoder(code, max_frames=frames, f_mode=fmode)
+    uh, _ = dec.decode(torch.from_numpy(llr).to(cuda), dev_words(u, cuda))
+    torch.cuda.synchronize()
+    cfg = dec.last_config
+    got_shape = (cfg["subtree_log2"], cfg["threads_per_cta"], cfg["ctas_per_frame"])
+    if sm_count() == 148:
+        assert got_shape == shape, f"{key}: launch shape {got_shape}, bench shape {shape}"
+    got = unpack_bits(uh.cpu().numpy().view(np.uint32), N)
+    ref = oracle(code, llr, u, fmode)
+    bad = np.flatnonzero(np.any(got != ref, axis=1))
+    assert bad.size == 0, f"{key}/{fmode} at {got_shape}: frames {bad[:10]} differ from the oracle"
+    # and the frame outcomes (FER) are the oracle's
+    assert np.array_equal(np.all(got == u, axis=1), np.all(ref == u, axis=1))
+
+
+@pytest.mark.parametrize("key", ["c3", "c4"])
+def test_launch_shape_determinism_sweep(cuda, key):
+    """Every cluster size x threads per CTA x sub-tree width decodes the same
+    u-hat as the oracle (fixed point; 8 frames of the config)."""
+    import torch
+    if key not in K.available_configs():
+        pytest.skip(f"{key}.pqct not built")
+    F = 8
+    code, x, u, llr = batch(key, F)
+    N = code.block_size
+    ref = oracle(code, llr, u, "fixed")
+    llr_d, u_d = torch.from_numpy(llr).to(cuda), dev_words(u, cuda)
+    dec = ScDecoder(code, max_frames=F, f_mode="fixed")
+    seen = set()
+    for ncl in (1, 2, 4, 8):
+        for nthr in (0, 64, 128, 256):
+            for lg in (11, 12, 13, 14):
+                dec.set_option(_lib.PQ_OPT_CLUSTER, ncl)
+                dec.set_option(_lib.PQ_OPT_THREADS, nthr)
+                dec.set_option(_lib.PQ_OPT_SUBTREE_LOG2, lg)
+                uh, _ = dec.decode(llr_d, u_d)
+                c = dec.last_config
+                seen.add((c["subtree_log2"], c["threads_per_cta"], c["ctas_per_frame"]))
+                got = unpack_bits(uh.cpu().numpy().view(np.uint32), N)
+                assert np.array_equal(got, ref), f"{key}: cluster {ncl} threads {nthr} S 2^{lg} differs"
+    assert any(t == 512 for _, t, _ in seen)  # the 512-thread cluster instantiation ran
+    assert len(seen) >= 40
+
+
+def test_exact_mode_shape_sweep(cuda):
+    """The exact (IEEE fp32) f at the bench shapes of c3 with forced clusters,
+    thread counts and sub-tree widths, against the fp32 mirror."""
+    import torch
+    if "c3" not in K.available_configs():
+        pytest.skip("c3.pqct not built")
+    F = 6
+    code, x, u, llr = batch("c3", F)
+    N = code.block_size
+    ref = oracle(code, llr, u, "exact")
+    llr_d, u_d = torch.from_numpy(llr).to(cuda), dev_words(u, cuda)
+    dec = ScDecoder(code, max_frames=F, f_mode="exact")
+    for ncl, nthr, lg in ((1, 256, 13), (1, 128, 11), (1, 64, 12), (2, 0, 13), (4, 0, 14), (8, 256, 11),
+                          (1, 256, 14)):
+        dec.set_option(_lib.PQ_OPT_CLUSTER, ncl)
+        dec.set_option(_lib.PQ_OPT_THREADS, nthr)
+        dec.set_option(_lib.PQ_OPT_SUBTREE_LOG2, lg)
+        uh, _ = dec.decode(llr_d, u_d)
+        got = unpack_bits(uh.cpu().numpy().view(np.uint32), N)
+        assert np.array_equal(got, ref), f"exact: cluster {ncl} threads {nthr} S 2^{lg} differs"
+
+
+def test_repeat_runs_identical(cuda):
+    """identical inputs give identical outputs across runs (five
+    decodes of the c3 bench batch through the fused BSC front end)."""
+    import torch
+    if "c3" not in K.available_configs():
+        pytest.skip("c3.pqct not built")
+    cfg = K.CONFIGS["c3"]
+    code = K.load_config("c3")
+    F, N = 64, code.block_size
+    x, llr, y = C.frames_batch(cfg.channel, cfg.seed, 0, F, N)
+    u = np.array([O.polar_transform_bytes(xi) for xi in x])
+    dec = ScDecoder(code, max_frames=F, f_mode="fixed")
+    outs = []
+    for _ in range(5):
+        uh, _ = dec.decode_bsc(dev_words(y, cuda), np.float32(cfg.channel.llr_magnitude), dev_words(u, cuda))
+        outs.append(uh.cpu().numpy())
+    for o in outs[1:]:
+        assert np.array_equal(o, outs[0])
+    ref = oracle(code, llr, u, "fixed")
+    assert np.array_equal(unpack_bits(outs[0].view(np.uint32), N), ref)

@@ -63,7 +63,7 @@ def test_argument_errors():
 
 def close_pe(got, ref):
     """Summation-order agreement, by pe band.  The reference convolves with an
-    FFT (construction.py:233) whose round-off (~1e-17 absolute per slot, kept
+    FFT (construction.py:231) whose round-off (~1e-17 absolute per slot, kept
     unless negative) dominates its densities' far tails, so pe of very good
     synthetic channels (< 1e-10, always information bits) is noise there; the
     GPU's direct convolution has none.  Measured: 1e-11 relative at pe >= 1e-2,

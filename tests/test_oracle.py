@@ -41,7 +41,7 @@ def test_phi_kats():
         O.phi(0.0)
 
 
-# ---- f pinned to the reference's own boxplus (construction.py:300-303)
+# ---- f pinned to the reference's own boxplus (construction.py:132-135)
 def test_f64_matches_reference_boxplus():
     g = golden("boxplus_grid.npz")
     ours = O.fmag64(g["a"], g["b"])

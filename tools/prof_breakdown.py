@@ -9,7 +9,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 import torch  # noqa: E402
 
-from bench import gen_frames  # noqa: E402
+from paper_1204_5882_b200.channel import frames_batch  # noqa: E402
 from paper_1204_5882_b200 import _lib  # noqa: E402
 from paper_1204_5882_b200 import codes as K  # noqa: E402
 from paper_1204_5882_b200.polar_core import ScDecoder, pack_bits, polar_transform_words  # noqa: E402
@@ -26,7 +26,7 @@ for key in a.configs:
     cfg = K.CONFIGS[key]
     code = K.load_config(key)
     F = a.frames or cfg.frames_per_gpu
-    x, llr, _ = gen_frames(cfg, code.block_size, 0, F)
+    x, llr, _ = frames_batch(cfg.channel, cfg.seed, 0, F, code.block_size, want_y=False)
     u = polar_transform_words(torch.from_numpy(pack_bits(x).view(np.int32).copy()).to(dev), code.n)
     dec = ScDecoder(code, max_frames=F, subtree_log2=a.subtree_log2, f_mode=a.fmode)
     dec.set_option(_lib.PQ_OPT_WARP_LOG2, a.warp_log2)

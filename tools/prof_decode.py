@@ -13,7 +13,7 @@ sys.path.insert(0, ROOT)
 
 import torch  # noqa: E402
 
-from bench import gen_frames  # noqa: E402
+from paper_1204_5882_b200.channel import frames_batch  # noqa: E402
 from paper_1204_5882_b200 import codes as K  # noqa: E402
 from paper_1204_5882_b200.polar_core import ScDecoder, pack_bits, polar_transform_words  # noqa: E402
 
@@ -28,7 +28,7 @@ a = ap.parse_args()
 cfg = K.CONFIGS[a.config]
 code = K.load_config(a.config)
 F = a.frames or cfg.frames_per_gpu
-x, llr, _ = gen_frames(cfg, code.block_size, 0, F)
+x, llr, _ = frames_batch(cfg.channel, cfg.seed, 0, F, code.block_size, want_y=False)
 dev = torch.device("cuda", 0)
 u = polar_transform_words(torch.from_numpy(pack_bits(x).view(np.int32).copy()).to(dev), code.n)
 dec = ScDecoder(code, max_frames=F, f_mode=a.fmode, ssc=not a.no_ssc, subtree_log2=a.subtree_log2)
