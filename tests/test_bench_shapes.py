@@ -6,7 +6,7 @@ test_gpu_parity.py run different shapes from the benchmark.  These tests decode
 the FULL BASELINE batches with automatic options -- exactly the shapes the bench
 times -- and compare every frame's u-hat with the oracle:
 
-  c2: 1024 frames -> 128-thread CTAs, 4 per SM, S = 2^11
+  c2: 1024 frames -> 128-thread CTAs, 4 per SM, S = 2^12
   c3, c4: 256 frames -> one CTA per frame, 256 threads, S = 2^13, TMA ring
   c5: 32 frames (N = 2^24) -> clusters of 4 CTAs, 512 threads, S = 2^14
 
@@ -28,7 +28,7 @@ pytestmark = pytest.mark.gpu
 
 # (frames, expected launch shape: subtree_log2, threads_per_cta, ctas_per_frame) on a 148-SM B200
 BENCH_SHAPES = {
-    "c2": (1024, (11, 128, 1)),
+    "c2": (1024, (12, 128, 1)),
     "c3": (256, (13, 256, 1)),
     "c4": (256, (13, 256, 1)),
     "c5": (32, (14, 512, 4)),
