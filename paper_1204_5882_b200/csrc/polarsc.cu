@@ -327,6 +327,12 @@ __constant__ float RATE1_TAU_FIX[26];
 template <int FM>
 __device__ __forceinline__ float tau(int k) { return FM == PQ_F_FIXED ? RATE1_TAU_FIX[k] : RATE1_TAU[k]; }
 
+// the fixed-point decoder's single-warp band (widths <= 2048)
+#include "serial_q88.cuh"
+#ifndef PQ_SE2
+#define PQ_SE2 1
+#endif
+
 template <int FM>
 __device__ __forceinline__ bool rate1_guard(float m, int k) { return m >= tau<FM>(k); }
 
@@ -351,6 +357,7 @@ struct DecParams {
     unsigned long long *prof;    // [F][PQ_PROF_SLOTS] clock64 cycles per step class, or null
     uint32_t wmax;               // widest node the single-warp band takes (32..256)
     uint32_t K;                  // CTAs per frame (a thread-block cluster; 1, 2, 4 or 8)
+    const uint32_t *fmask;       // [wpf] frozen mask words (bit i = leaf i frozen), shared by frames
 };
 
 // step classes for the optional per-frame cycle profile (PQ_OPT_PROFILE)
@@ -415,11 +422,12 @@ __device__ __forceinline__ float4 chan_load4(const DecParams &p, const FrameCtx 
     return v;
 }
 
-// smem layout: [2S floats stage LLRs][SW words partial sums][2S bytes types]
+// smem layout: [2S floats stage LLRs][SW words partial sums][2S bytes types][SW words frozen mask]
 struct Smem {
     float *st;
     uint32_t *xs;
     uint8_t *ty;
+    uint32_t *fm;  // frozen-mask words of the current S-sub-tree (fixed-point serial engine)
 };
 
 // stage pointer for a node of width W at depth d >= 1
@@ -1669,10 +1677,14 @@ __global__ void __launch_bounds__(NT, NT == 512 ? 1 : 2) sc_decode_kernel(DecPar
     sm.xs = (uint32_t *)(sm.st + 2 * S);
     const uint32_t SW = S >= 32 ? S / 32 : 1;
     sm.ty = (uint8_t *)(sm.xs + SW);
+    sm.fm = (uint32_t *)(sm.ty + 2 * S);
+    const bool se2 = FM == PQ_F_FIXED && PQ_SE2 && !p.plain && p.dump == nullptr;
 
     load_log_table();
-    if (FM == PQ_F_FIXED)
+    if (FM == PQ_F_FIXED) {
         for (int i = threadIdx.x; i < CORR_SMEM; i += blockDim.x) pq_corrtab[i] = CORR_TAB_C[i];
+        if (PQ_SE2) se::load_tables();
+    }
     __syncthreads();
     const uint32_t K = CL ? p.K : 1u;  // CL = false: the single-CTA path compiles without slicing
     const uint32_t rank = blockIdx.x & (K - 1);  // CTA rank in the frame's cluster
@@ -1832,6 +1844,8 @@ __global__ void __launch_bounds__(NT, NT == 512 ? 1 : 2) sc_decode_kernel(DecPar
                         sm.ty[q] = __ldg(p.types + ((size_t)1 << (dS + e)) + ((size_t)j << e) + (q - (1u << e)));
                     }
                 }
+                if (se2 && S >= 32)
+                    for (uint32_t w = tid; w < S / 32; w += nthr) sm.fm[w] = __ldg(p.fmask + (size_t)j * (S / 32) + w);
                 __syncthreads();  // the types are read right below (before the next step's barrier)
             }
             if (W <= WMAX) {
@@ -1852,7 +1866,9 @@ __global__ void __launch_bounds__(NT, NT == 512 ? 1 : 2) sc_decode_kernel(DecPar
 #ifndef PQ_WALK2
 #define PQ_WALK2 1
 #endif
-                        if (!p.plain && fc.dump == nullptr && W > 512)
+                        if (se2)
+                            se::root(sm.st + 2 * S, sm.xs, sm.ty, sm.fm, S, dS, d, j);
+                        else if (!p.plain && fc.dump == nullptr && W > 512)
                             warp_wide_root<FM>(sm.st + 2 * S, sm.xs, sm.ty, S, dS, d, j);
                         else if (PQ_WALK2 && !p.plain && fc.dump == nullptr && W >= 64)
                             warp_walk2<FM>(sm.st + 2 * S, sm.xs, sm.ty, S, dS, d, j);
@@ -2327,6 +2343,10 @@ static int choose_K(const pq_decoder *h, int frames, int log2S, bool dump)
 template <int FM>
 static int launch_dec(const DecParams &p, int frames, int nthreads, size_t smem, cudaStream_t st)
 {
+#ifdef PQ_NO_DECODE_KERNELS
+    // microbenchmarks that include this file for its device functions only
+    return set_err(-1, "built without the decode kernels");
+#else
     const bool diag = p.plain || p.dump || p.prof;
     if (p.K == 1) {
         auto kern = diag ? sc_decode_kernel<FM, false, true, 256> : sc_decode_kernel<FM, false, false, 256>;
@@ -2353,6 +2373,7 @@ static int launch_dec(const DecParams &p, int frames, int nthreads, size_t smem,
     cfg.numAttrs = 1;
     CUDA_TRY(cudaLaunchKernelEx(&cfg, ckern, p));
     return 0;
+#endif
 }
 
 // threads per CTA: 256 when frames leave <= 2 per SM (latency: a frame's
@@ -2381,7 +2402,9 @@ static int choose_log2S(const pq_decoder *h, int frames, int nthreads)
     int best = 6;
     for (int k = 6; k <= 14; k++) {
         const size_t S = (size_t)1 << k;
-        const size_t bytes = 8 * S + (S / 32) * 4 + 2 * S + 10 * 1024;  // + static (table, barriers)
+        // dynamic (stage LLRs, partial sums, types, frozen-mask words) + static
+        // (tables, barriers; the fixed-point serial engine's 4 KB byte table)
+        const size_t bytes = 8 * S + (S / 32) * 8 + 2 * S + 10 * 1024 + (h->fmode == PQ_F_FIXED ? 4096 : 0);
         if ((size_t)per_sm * bytes <= 226 * 1024) best = k;
     }
     if (best > h->n) best = h->n;
@@ -2391,7 +2414,7 @@ static int choose_log2S(const pq_decoder *h, int frames, int nthreads)
 static size_t dec_smem_bytes(uint32_t S)
 {
     const uint32_t SW = S >= 32 ? S / 32 : 1;
-    return (size_t)8 * S + (size_t)SW * 4 + (size_t)2 * S;
+    return (size_t)8 * S + (size_t)SW * 4 + (size_t)2 * S + (size_t)SW * 4;
 }
 
 // Q8.8 phi table and the fixed-point rate-1 thresholds, computed
@@ -2450,6 +2473,9 @@ static int ensure_fixed_tables()
     fixed_tables(corr, tau);
     CUDA_TRY(cudaMemcpyToSymbol(CORR_TAB_C, corr, sizeof corr));
     CUDA_TRY(cudaMemcpyToSymbol(RATE1_TAU_FIX, tau, sizeof tau));
+    int taui[26];
+    for (int k = 0; k < 26; k++) taui[k] = tau[k] > 1e9f ? INT_MAX : (int)tau[k];
+    CUDA_TRY(cudaMemcpyToSymbol(se::TAUI, taui, sizeof taui));
     // pageable uploads may return before the DMA lands; a decode on a
     // non-blocking stream is not ordered after them, so wait here once
     CUDA_TRY(cudaDeviceSynchronize());
@@ -2748,6 +2774,7 @@ static int decode_impl(pq_decoder *h, const float *llr, const uint32_t *ybits, f
     p.mag = mag;
     p.cw = cw;
     p.types = h->d_types;
+    p.fmask = h->d_mask;
     p.scr = h->d_scr;
     p.X = h->d_x;
     p.dump = dump;

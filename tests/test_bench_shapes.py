@@ -161,3 +161,24 @@ def test_repeat_runs_identical(cuda):
         assert np.array_equal(o, outs[0])
     ref = oracle(code, llr, u, "fixed")
     assert np.array_equal(unpack_bits(outs[0].view(np.uint32), N), ref)
+
+
+@pytest.mark.parametrize("warp_log2", [5, 6, 7, 8, 9])
+def test_fixed_serial_band_widths(cuda, warp_log2):
+    """The fixed-point serial engine entered at every width the warp band can
+    start at (PQ_OPT_WARP_LOG2 5..9, plus the default 2048) on a random code
+    and on c4's frozen set, against the integer oracle."""
+    import torch
+    rng = np.random.default_rng(40 + warp_log2)
+    for n, frac in ((13, 0.45), (14, 0.3)):
+        N = 1 << n
+        mask = (rng.random(N) < frac).astype(np.uint8)
+        code = K.PolarCode(n=n, frozen_mask=mask, channel=C.BiAwgn(1.0), target_fer=0.1)
+        F = 4
+        llr = rng.normal(1.0, 2.2, (F, N)).astype(np.float32)
+        fz = rng.integers(0, 2, (F, N)).astype(np.uint8)
+        ref = oracle(code, llr, fz, "fixed")
+        dec = ScDecoder(code, max_frames=F, f_mode="fixed")
+        dec.set_option(_lib.PQ_OPT_WARP_LOG2, warp_log2)
+        uh, _ = dec.decode(torch.from_numpy(llr).to(cuda), dev_words(fz, cuda))
+        assert np.array_equal(unpack_bits(uh.cpu().numpy().view(np.uint32), N), ref)
