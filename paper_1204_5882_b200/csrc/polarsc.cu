@@ -328,6 +328,9 @@ template <int FM>
 __device__ __forceinline__ float tau(int k) { return FM == PQ_F_FIXED ? RATE1_TAU_FIX[k] : RATE1_TAU[k]; }
 
 // the fixed-point decoder's single-warp band (widths <= 2048)
+#ifndef PQ_WIDE_WARP_LOG2
+#define PQ_WIDE_WARP_LOG2 11  // widest node the serial warp takes (wider: block steps)
+#endif
 #include "serial_q88.cuh"
 #ifndef PQ_SE2
 #define PQ_SE2 1
@@ -1293,9 +1296,6 @@ __device__ __noinline__ void warp_walk2(float *st_end, uint32_t *xs, const uint8
 // per lane per step, independent), and hands the 512-wide children to
 // warp_walk2 -- no block barriers and no trip through the block-level main
 // loop for these nodes
-#ifndef PQ_WIDE_WARP_LOG2
-#define PQ_WIDE_WARP_LOG2 11
-#endif
 template <int FM, int W>
 __device__ __forceinline__ void warp_wide(float *st_end, uint32_t *xs, const uint8_t *ty, uint32_t S, int dS, int d0,
                                           uint32_t j0)
@@ -2802,9 +2802,13 @@ static int decode_impl(pq_decoder *h, const float *llr, const uint32_t *ybits, f
     if (h->timing) CUDA_TRY(cudaEventRecord(h->ev[2 * slot], st));
     int lrc;
     if (h->fmode == PQ_F_FIXED) lrc = launch_dec<PQ_F_FIXED>(p, frames, nthreads, smem, st);
+#ifdef PQ_ONLY_FIXED  // A/B builds of the fixed-point kernel (tools/build_variant.sh)
+    else lrc = set_err(-1, "variant build: fixed point only");
+#else
     else if (h->fmode == PQ_F_MINSUM) lrc = launch_dec<PQ_F_MINSUM>(p, frames, nthreads, smem, st);
     else if (h->fmode == PQ_F_FAST) lrc = launch_dec<PQ_F_FAST>(p, frames, nthreads, smem, st);
     else lrc = launch_dec<PQ_F_EXACT>(p, frames, nthreads, smem, st);
+#endif
     if (lrc) return lrc;
     if (h->timing) {
         CUDA_TRY(cudaEventRecord(h->ev[2 * slot + 1], st));

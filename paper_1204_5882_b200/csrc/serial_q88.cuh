@@ -40,7 +40,13 @@
 #define SE_W8_PATTERNS 2
 #endif
 #ifndef SE_UNR
-#define SE_UNR 512  // widest node of the compile-time unrolled register walk
+#define SE_UNR 256  // widest node of the compile-time unrolled register walk
+#endif
+#ifndef SE_TREE
+#define SE_TREE 0
+#endif
+#ifndef SE_WIDE_COMPACT
+#define SE_WIDE_COMPACT 0
 #endif
 #ifndef SE_SPEC_LP
 #define SE_SPEC_LP 0
@@ -611,14 +617,38 @@ __device__ __forceinline__ void wide(float *st_end, uint32_t *xs, const uint8_t 
         }
     }
     if (t == T_REP) {
-        int acc[V];
+        int s0;
+        if constexpr (V <= 64) {
+            int acc[V];
 #pragma unroll
-        for (int q = 0; q < V; q++) acc[q] = ld(32 * q + lane);
+            for (int q = 0; q < V; q++) acc[q] = ld(32 * q + lane);
 #pragma unroll
-        for (int hv = V / 2; hv >= 1; hv >>= 1)
+            for (int hv = V / 2; hv >= 1; hv >>= 1)
 #pragma unroll
-            for (int q = 0; q < hv; q++) acc[q] = qa(acc[q + hv], acc[q]);
-        int s0 = acc[0];
+                for (int q = 0; q < hv; q++) acc[q] = qa(acc[q + hv], acc[q]);
+            s0 = acc[0];
+        } else {
+            // very wide repetition node (rare): fold in SC's pairing order
+            // through the free child stage area, then in registers
+#pragma unroll 1
+            for (int hv = V / 2; hv >= 32; hv >>= 1)
+#pragma unroll 1
+                for (int q = 0; q < hv; q++) {
+                    const int a = hv == V / 2 ? ld(32 * q + lane) : ch[32 * q + lane];
+                    const int b = hv == V / 2 ? ld(32 * (q + hv) + lane) : ch[32 * (q + hv) + lane];
+                    __syncwarp();
+                    ch[32 * q + lane] = qa(b, a);
+                    __syncwarp();
+                }
+            int acc[32];
+#pragma unroll
+            for (int q = 0; q < 32; q++) acc[q] = ch[32 * q + lane];
+#pragma unroll
+            for (int hv = 16; hv >= 1; hv >>= 1)
+#pragma unroll
+                for (int q = 0; q < hv; q++) acc[q] = qa(acc[q + hv], acc[q]);
+            s0 = acc[0];
+        }
 #pragma unroll
         for (int hh = 16; hh >= 1; hh >>= 1) s0 = qa(__shfl_down_sync(FULL, s0, hh), s0);
         const uint32_t bits = __shfl_sync(FULL, s0, 0) < 0 ? FULL : 0u;
@@ -642,7 +672,7 @@ __device__ __forceinline__ void wide(float *st_end, uint32_t *xs, const uint8_t 
             for (int k = 0; k < B; k++) ch[32 * (q0 + k) + lane] = fq(a[k], b[k]);
         }
         __syncwarp();
-        if constexpr (W / 2 > 512) wide<W / 2, false>(st_end, xs, ty, fm, S, dS, d0 + 1, 2 * j0);
+        if constexpr (W / 2 > SE_UNR) wide<W / 2, false>(st_end, xs, ty, fm, S, dS, d0 + 1, 2 * j0);
         else walk(reinterpret_cast<const int *>(st_end - W), xs, ty, fm, S, dS, d0 + 1, 2 * j0);
     }
     if (tr == T_R0) {
@@ -663,11 +693,265 @@ __device__ __forceinline__ void wide(float *st_end, uint32_t *xs, const uint8_t 
             for (int k = 0; k < B; k++) ch[32 * (q0 + k) + lane] = gq(a[k], b[k], (sw[k] >> lane) & 1u);
         }
         __syncwarp();
-        if constexpr (W / 2 > 512) wide<W / 2, false>(st_end, xs, ty, fm, S, dS, d0 + 1, 2 * j0 + 1);
+        if constexpr (W / 2 > SE_UNR) wide<W / 2, false>(st_end, xs, ty, fm, S, dS, d0 + 1, 2 * j0 + 1);
         else walk(reinterpret_cast<const int *>(st_end - W), xs, ty, fm, S, dS, d0 + 1, 2 * j0 + 1);
     }
     for (int q = lane; q < Vh; q += 32) xw[q] ^= xw[Vh + q];
     __syncwarp();
+}
+
+// compact variant of wide (SE_WIDE_COMPACT): one out-of-line copy per width,
+// the two children through one loop body, the node already int.  Smaller
+// code: the band is re-entered ~300 times per N = 2^20 frame after block and
+// upper-band steps have evicted its instructions from the SM's caches.
+template <int W>
+__device__ __noinline__ void widec(float *st_end, uint32_t *xs, const uint8_t *ty, const uint32_t *fm, uint32_t S,
+                                   int dS, int d0, uint32_t j0)
+{
+    constexpr int V = W / 32, Vh = V / 2, B = 8;
+    const unsigned FULL = 0xffffffffu;
+    const int lane = threadIdx.x & 31;
+    const int e = d0 - dS;
+    const uint32_t lh = (1u << e) + (j0 & ((1u << e) - 1u));
+    const int *nd = reinterpret_cast<const int *>(st_end - 2 * W);
+    int *ch = reinterpret_cast<int *>(st_end - W);
+    uint32_t *xw = xs + (((j0 * W) & (S - 1)) >> 5);
+    const uint8_t t = ty[lh];
+    if (t == T_R0) {
+        for (int q = lane; q < V; q += 32) xw[q] = 0u;
+        __syncwarp();
+        return;
+    }
+    if (t == T_R1) {
+        int mn = 0x7fffffff;
+#pragma unroll 1
+        for (int q0 = 0; q0 < V; q0 += B) {
+            int a[B];
+#pragma unroll
+            for (int k = 0; k < B; k++) a[k] = nd[32 * (q0 + k) + lane];
+#pragma unroll
+            for (int k = 0; k < B; k++) mn = min(mn, abs(a[k]));
+        }
+        if (__all_sync(FULL, mn >= TAUI[clog2(W)])) {
+#pragma unroll 1
+            for (int q0 = 0; q0 < V; q0 += B) {
+                int a[B];
+#pragma unroll
+                for (int k = 0; k < B; k++) a[k] = nd[32 * (q0 + k) + lane];
+                uint32_t w = 0;
+#pragma unroll
+                for (int k = 0; k < B; k++) {
+                    const uint32_t b = __ballot_sync(FULL, a[k] < 0);
+                    w = lane == k ? b : w;
+                }
+                if (lane < B) xw[q0 + lane] = w;
+            }
+            __syncwarp();
+            return;
+        }
+    }
+    if (t == T_REP) {
+        // SC's pairing order: fold the in-lane levels through the free child
+        // area, then the lanes
+#pragma unroll 1
+        for (int hv = V / 2; hv >= 1; hv >>= 1)
+#pragma unroll 1
+            for (int q = 0; q < hv; q++) {
+                const int a = hv == V / 2 ? nd[32 * q + lane] : ch[32 * q + lane];
+                const int b = hv == V / 2 ? nd[32 * (q + hv) + lane] : ch[32 * (q + hv) + lane];
+                __syncwarp();
+                ch[32 * q + lane] = qa(b, a);
+                __syncwarp();
+            }
+        int s0 = ch[lane];
+#pragma unroll
+        for (int hh = 16; hh >= 1; hh >>= 1) s0 = qa(__shfl_down_sync(FULL, s0, hh), s0);
+        const uint32_t bits = __shfl_sync(FULL, s0, 0) < 0 ? FULL : 0u;
+        for (int q = lane; q < V; q += 32) xw[q] = bits;
+        __syncwarp();
+        return;
+    }
+#pragma unroll 1
+    for (int side = 0; side < 2; side++) {
+        if (ty[2 * lh + side] == T_R0) {
+            for (int q = lane; q < Vh; q += 32) xw[side * Vh + q] = 0u;
+            __syncwarp();
+            continue;
+        }
+#pragma unroll 1
+        for (int q0 = 0; q0 < Vh; q0 += B) {
+            int a[B], b[B];
+            uint32_t sw[B];
+#pragma unroll
+            for (int k = 0; k < B; k++) {
+                a[k] = nd[32 * (q0 + k) + lane];
+                b[k] = nd[32 * (q0 + k) + lane + W / 2];
+                sw[k] = side ? xw[q0 + k] : 0u;
+            }
+            if (side) {
+#pragma unroll
+                for (int k = 0; k < B; k++) ch[32 * (q0 + k) + lane] = gq(a[k], b[k], (sw[k] >> lane) & 1u);
+            } else {
+#pragma unroll
+                for (int k = 0; k < B; k++) ch[32 * (q0 + k) + lane] = fq(a[k], b[k]);
+            }
+        }
+        __syncwarp();
+        if constexpr (W / 2 > SE_UNR) widec<W / 2>(st_end, xs, ty, fm, S, dS, d0 + 1, 2 * j0 + side);
+        else walk(reinterpret_cast<const int *>(st_end - W), xs, ty, fm, S, dS, d0 + 1, 2 * j0 + side);
+    }
+    for (int q = lane; q < Vh; q += 32) xw[q] ^= xw[Vh + q];
+    __syncwarp();
+}
+
+// ---- widths above SE_UNR, iterative form (SE_TREE): a walk over the
+// shared-memory stage buffers (node of width W at st_end - 2W, int codes) with
+// one copy of each step for every width -- no per-position copies and no
+// calls per node (the band is re-entered ~300 times per 2^20 frame after
+// block and upper-band steps have evicted its instructions).  Every loop
+// loads a batch before it computes or stores (one shared array: unbatched,
+// each element's loads would wait for the previous element's store).
+__device__ __noinline__ void tree(float *st_end, uint32_t *xs, const uint8_t *ty, const uint32_t *fm, uint32_t S,
+                                  int dS, int d0, uint32_t j0)
+{
+    constexpr int B = 8;
+    const unsigned FULL = 0xffffffffu;
+    const int lane = threadIdx.x & 31;
+    int d = d0;
+    uint32_t j = j0;
+    bool entering = true;
+    for (;;) {
+        const uint32_t W = S >> (d - dS);
+        const int V = (int)(W >> 5), lgW = 31 - __clz(W);
+        const int e = d - dS;
+        const uint32_t lh = (1u << e) + (j & ((1u << e) - 1u));
+        int *nd = reinterpret_cast<int *>(st_end - 2 * W);
+        uint32_t *xw = xs + (((j * W) & (S - 1)) >> 5);
+        if (entering) {
+            entering = false;
+            if (W <= SE_UNR) {
+                walk(nd, xs, ty, fm, S, dS, d, j);
+                continue;
+            }
+            const uint8_t t = ty[lh];
+            if (t == T_R0) {
+                for (int q = lane; q < V; q += 32) xw[q] = 0u;
+                __syncwarp();
+                continue;
+            }
+            if (t == T_R1) {
+                int mn = 0x7fffffff;
+#pragma unroll 1
+                for (int q0 = 0; q0 < V; q0 += B) {
+                    int a[B];
+#pragma unroll
+                    for (int k = 0; k < B; k++) a[k] = q0 + k < V ? nd[32 * (q0 + k) + lane] : 0x7fffffff;
+#pragma unroll
+                    for (int k = 0; k < B; k++) mn = min(mn, abs(a[k]));
+                }
+                if (__all_sync(FULL, mn >= TAUI[lgW])) {
+#pragma unroll 1
+                    for (int q0 = 0; q0 < V; q0 += B) {
+                        int a[B];
+#pragma unroll
+                        for (int k = 0; k < B; k++) a[k] = q0 + k < V ? nd[32 * (q0 + k) + lane] : 0;
+                        uint32_t w = 0;
+#pragma unroll
+                        for (int k = 0; k < B; k++) {
+                            const uint32_t b = __ballot_sync(FULL, a[k] < 0);
+                            w = lane == k ? b : w;
+                        }
+                        if (lane < B && q0 + lane < V) xw[q0 + lane] = w;
+                    }
+                    __syncwarp();
+                    continue;
+                }
+            }
+            if (t == T_REP) {
+                // SC's pairing order: fold the in-lane levels through the free
+                // child area, then the lanes
+                int *tmp = reinterpret_cast<int *>(st_end - W);
+#pragma unroll 1
+                for (int hv = V / 2; hv >= 1; hv >>= 1)
+#pragma unroll 1
+                    for (int q = 0; q < hv; q++) {
+                        const int *src = hv == V / 2 ? nd : tmp;
+                        const int a = src[32 * q + lane], b = src[32 * (q + hv) + lane];
+                        __syncwarp();
+                        tmp[32 * q + lane] = qa(b, a);
+                        __syncwarp();
+                    }
+                int acc = tmp[lane];
+#pragma unroll
+                for (int hh = 16; hh >= 1; hh >>= 1) acc = qa(__shfl_down_sync(FULL, acc, hh), acc);
+                const uint32_t bits = __shfl_sync(FULL, acc, 0) < 0 ? FULL : 0u;
+                for (int q = lane; q < V; q += 32) xw[q] = bits;
+                __syncwarp();
+                continue;
+            }
+            // mixed (or a rate-1 node whose guard failed): f-step into the left child
+            d++;
+            j = 2 * j;
+            if (ty[2 * lh] == T_R0) {
+                for (int q = lane; q < V / 2; q += 32) xw[q] = 0u;
+                __syncwarp();
+                continue;  // the left child is decided
+            }
+            int *ch = reinterpret_cast<int *>(st_end - W);
+            const int Vh = V / 2;
+#pragma unroll 1
+            for (int q0 = 0; q0 < Vh; q0 += B) {
+                int a[B], b[B];
+#pragma unroll
+                for (int k = 0; k < B; k++) {
+                    a[k] = nd[32 * (q0 + k) + lane];
+                    b[k] = nd[32 * (q0 + k) + lane + W / 2];
+                }
+#pragma unroll
+                for (int k = 0; k < B; k++)
+                    if (q0 + k < Vh) ch[32 * (q0 + k) + lane] = fq(a[k], b[k]);
+            }
+            __syncwarp();
+            entering = true;
+            continue;
+        }
+        // ---- node (d, j) is decided
+        if (d == d0) break;
+        if ((j & 1u) == 0) {
+            // left child done -> g-step at the parent into the right child
+            j = j + 1;
+            uint32_t *xr = xw + V;
+            if (ty[lh + 1] == T_R0) {
+                for (int q = lane; q < V; q += 32) xr[q] = 0u;
+                __syncwarp();
+                continue;  // the right child is decided
+            }
+            const int *pa = reinterpret_cast<const int *>(st_end - 4 * W);  // the parent (width 2W)
+#pragma unroll 1
+            for (int q0 = 0; q0 < V; q0 += B) {
+                int a[B], b[B];
+                uint32_t sw[B];
+#pragma unroll
+                for (int k = 0; k < B; k++) {
+                    a[k] = pa[32 * (q0 + k) + lane];
+                    b[k] = pa[32 * (q0 + k) + lane + W];
+                    sw[k] = xw[q0 + k];
+                }
+#pragma unroll
+                for (int k = 0; k < B; k++)
+                    if (q0 + k < V) nd[32 * (q0 + k) + lane] = gq(a[k], b[k], (sw[k] >> lane) & 1u);
+            }
+            __syncwarp();
+            entering = true;
+            continue;
+        }
+        // right child done -> the parent's partial sums (xl ^ xr, xr)
+        uint32_t *xl = xw - V;
+        for (int q = lane; q < V; q += 32) xl[q] ^= xw[q];
+        __syncwarp();
+        d--;
+        j >>= 1;
+    }
 }
 
 // Entry: the node (d0, j0) of width W = S >> (d0 - dS), 32 <= W <= 2048, whose
@@ -679,10 +963,84 @@ __device__ __noinline__ void root(float *st_end, uint32_t *xs, const uint8_t *ty
 {
     const int lane = threadIdx.x & 31;
     const uint32_t W = S >> (d0 - dS);
-    if (W == 2048) {
+#if SE_TREE
+    if (W >= 64) {
+        // the node's fp32 codes -> int in place (batched: loads ahead of stores)
+        float *nd = st_end - 2 * W;
+#pragma unroll 1
+        for (uint32_t i0 = 0; i0 < W; i0 += 256) {
+            float a[8];
+#pragma unroll
+            for (int k = 0; k < 8; k++) a[k] = i0 + 32 * k < W ? nd[i0 + 32 * k + lane] : 0.0f;
+#pragma unroll
+            for (int k = 0; k < 8; k++)
+                if (i0 + 32 * k < W) reinterpret_cast<int *>(nd)[i0 + 32 * k + lane] = f2q(a[k]);
+        }
+        __syncwarp();
+        if (W > SE_UNR) tree(st_end, xs, ty, fm, S, dS, d0, j0);
+        else walk(reinterpret_cast<const int *>(nd), xs, ty, fm, S, dS, d0, j0);
+#elif SE_WIDE_COMPACT
+    if (W >= 64) {
+        // the node's fp32 codes -> int in place (batched: loads ahead of stores)
+        float *nd = st_end - 2 * W;
+#pragma unroll 1
+        for (uint32_t i0 = 0; i0 < W; i0 += 256) {
+            float a[8];
+#pragma unroll
+            for (int k = 0; k < 8; k++) a[k] = i0 + 32 * k < W ? nd[i0 + 32 * k + lane] : 0.0f;
+#pragma unroll
+            for (int k = 0; k < 8; k++)
+                if (i0 + 32 * k < W) reinterpret_cast<int *>(nd)[i0 + 32 * k + lane] = f2q(a[k]);
+        }
+        __syncwarp();
+        if (W > SE_UNR) {
+            if (false) {
+#if PQ_WIDE_WARP_LOG2 >= 12
+            } else if (W == 4096) {
+                widec<4096>(st_end, xs, ty, fm, S, dS, d0, j0);
+#endif
+            } else if (W == 2048) {
+                widec<2048>(st_end, xs, ty, fm, S, dS, d0, j0);
+            } else if (W == 1024) {
+                widec<1024>(st_end, xs, ty, fm, S, dS, d0, j0);
+#if SE_UNR < 512
+            } else if (W == 512) {
+                widec<512>(st_end, xs, ty, fm, S, dS, d0, j0);
+#endif
+#if SE_UNR < 256
+            } else {
+                widec<256>(st_end, xs, ty, fm, S, dS, d0, j0);
+#endif
+            }
+        } else {
+            walk(reinterpret_cast<const int *>(nd), xs, ty, fm, S, dS, d0, j0);
+        }
+#else
+    if (false) {
+#if PQ_WIDE_WARP_LOG2 >= 14
+    } else if (W == 16384) {
+        wide<16384, true>(st_end, xs, ty, fm, S, dS, d0, j0);
+#endif
+#if PQ_WIDE_WARP_LOG2 >= 13
+    } else if (W == 8192) {
+        wide<8192, true>(st_end, xs, ty, fm, S, dS, d0, j0);
+#endif
+#if PQ_WIDE_WARP_LOG2 >= 12
+    } else if (W == 4096) {
+        wide<4096, true>(st_end, xs, ty, fm, S, dS, d0, j0);
+#endif
+    } else if (W == 2048) {
         wide<2048, true>(st_end, xs, ty, fm, S, dS, d0, j0);
     } else if (W == 1024) {
         wide<1024, true>(st_end, xs, ty, fm, S, dS, d0, j0);
+#if SE_UNR < 512
+    } else if (W == 512) {
+        wide<512, true>(st_end, xs, ty, fm, S, dS, d0, j0);
+#endif
+#if SE_UNR < 256
+    } else if (W == 256) {
+        wide<256, true>(st_end, xs, ty, fm, S, dS, d0, j0);
+#endif
     } else if (W >= 64) {
         // the node's fp32 codes -> int in place (batched: loads ahead of stores)
         float *nd = st_end - 2 * W;
@@ -697,6 +1055,7 @@ __device__ __noinline__ void root(float *st_end, uint32_t *xs, const uint8_t *ty
         }
         __syncwarp();
         walk(reinterpret_cast<const int *>(nd), xs, ty, fm, S, dS, d0, j0);
+#endif
     } else {
         const uint32_t pos = (j0 * W) & (S - 1);
         const uint32_t bits = w32(f2q((st_end - 64)[lane]), fm[pos >> 5]);
