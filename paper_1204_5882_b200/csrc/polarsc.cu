@@ -51,6 +51,37 @@
 #include "../../include/polarsc.h"
 
 // ---------------------------------------------------------------------------
+// PQ_CHECKED builds (tools/checked_build.sh; compute-sanitizer is not
+// available on the GPU pool): device-side bounds asserts on the shared-memory
+// and scratch indices, shared memory poisoned (NaN) at kernel start, and
+// per-warp random delays at every step of the tree walk and of the TMA ring,
+// so that a missing barrier or fence shows up as a parity mismatch or a
+// nondeterministic result across runs.
+#ifdef PQ_CHECKED
+__device__ __forceinline__ uint32_t pq_hash32(uint32_t x)
+{
+    x ^= x >> 16; x *= 0x7feb352du; x ^= x >> 15; x *= 0x846ca68bu; x ^= x >> 16;
+    return x;
+}
+#define PQ_CHECK(cond)                                                                                 \
+    do {                                                                                               \
+        if (!(cond)) {                                                                                 \
+            printf("PQ_CHECK failed: %s at %s:%d (block %d thread %d)\n", #cond, __FILE__, __LINE__,   \
+                   (int)blockIdx.x, (int)threadIdx.x);                                                 \
+            __trap();                                                                                  \
+        }                                                                                              \
+    } while (0)
+#define PQ_JITTER()                                                                                     \
+    do {                                                                                               \
+        const uint32_t h_ = pq_hash32((uint32_t)clock() ^ (threadIdx.x >> 5) * 0x9e3779b9u ^ blockIdx.x); \
+        if ((h_ & 3u) == 0u) __nanosleep(h_ >> 22);                                                    \
+    } while (0)
+#else
+#define PQ_CHECK(cond) ((void)0)
+#define PQ_JITTER() ((void)0)
+#endif
+
+// ---------------------------------------------------------------------------
 // error plumbing
 
 static thread_local std::string g_last_error;
@@ -437,6 +468,7 @@ struct Smem {
 __device__ __forceinline__ float *stage_ptr(const DecParams &p, const FrameCtx &fc, const Smem &sm,
                                             uint32_t W)
 {
+    PQ_CHECK(W >= 1 && W <= p.N && (W & (W - 1)) == 0 && (W <= p.S || fc.scr != nullptr));
     return W <= p.S ? sm.st + (2 * p.S - 2 * W) : fc.scr + (p.N - 2 * W);
 }
 
@@ -1591,6 +1623,7 @@ __device__ __forceinline__ void ring_step(const DecParams &p, const Ring &r, con
         for (uint32_t c = 0; c < nch && c < D; c++) ring_issue(r, u, lo + c * C, c, ef);
     uint32_t s = 0;
     for (uint32_t c = 0; c < nch; c++) {
+        PQ_JITTER();
         mbar_wait(&r.bar[s], (ph >> s) & 1u);
         ph ^= 1u << s;
         const unsigned char *st = reinterpret_cast<const unsigned char *>(r.base) + (size_t)s * r.sbytes;
@@ -1672,6 +1705,14 @@ __global__ void __launch_bounds__(NT, NT == 512 ? 1 : 2) sc_decode_kernel(DecPar
     extern __shared__ __align__(16) unsigned char smem_raw[];
     __shared__ float red[32];
     const uint32_t S = p.S, N = p.N;
+#ifdef PQ_CHECKED
+    {
+        uint32_t dyn;
+        asm volatile("mov.u32 %0, %%dynamic_smem_size;" : "=r"(dyn));
+        for (uint32_t i = threadIdx.x; i < dyn / 4; i += blockDim.x) reinterpret_cast<uint32_t *>(smem_raw)[i] = 0x7fc00001u;
+        __syncthreads();
+    }
+#endif
     Smem sm;
     sm.st = (float *)smem_raw;
     sm.xs = (uint32_t *)(sm.st + 2 * S);
@@ -1802,6 +1843,7 @@ __global__ void __launch_bounds__(NT, NT == 512 ? 1 : 2) sc_decode_kernel(DecPar
         }                                                      \
     } while (0)
     for (;;) {
+        PQ_JITTER();
         const uint32_t W = N >> d;
         if (entering) {
             if (!lead && W <= S) {  // the leader decodes it; wait at the next cluster barrier

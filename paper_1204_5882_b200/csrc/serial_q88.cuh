@@ -422,6 +422,7 @@ __device__ __forceinline__ void wchild(const int (&x)[H / 32], const WalkCtx &c,
         // relative heap position REL at the width-32 level: leaf offset
         constexpr int e = clog2(REL);
         const uint32_t pos = c.pos0 + 32u * (uint32_t)(REL - (1 << e));
+        PQ_CHECK(e >= 0 && REL < 32);
         xo[0] = w32(x[0], c.fm[pos >> 5]);
     } else {
         wnode<H, REL>(x, c, xo);
@@ -963,6 +964,8 @@ __device__ __noinline__ void root(float *st_end, uint32_t *xs, const uint8_t *ty
 {
     const int lane = threadIdx.x & 31;
     const uint32_t W = S >> (d0 - dS);
+    PQ_CHECK(W >= 32 && W <= S && d0 >= dS && ((j0 * W) & (S - 1)) + W <= S);
+    PQ_JITTER();
 #if SE_TREE
     if (W >= 64) {
         // the node's fp32 codes -> int in place (batched: loads ahead of stores)
