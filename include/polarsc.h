@@ -170,6 +170,21 @@ int pq_de_run(pq_de *h, const double *base_density, int n, double prune_z_eps, d
               double mass_floor, double *pe_out);
 int pq_de_destroy(pq_de *h);
 
+/* Read a PQCT code-table file -- the reference's binary frozen-set format.
+ * Replaces: read_code_table(path) (construction.py:483-507), with its
+ * BLAKE2b-64 checksum (construction.py:458-459) and the same rejections
+ * (return codes: -3 "code table truncated", -4 "bad code-table magic",
+ * -5 "code-table checksum mismatch", -6 "unsupported code-table version",
+ * -2 unreadable file, -1 bad arguments; the text is in pq_last_error()).
+ * Outputs are nullable; mask_out (mask_len >= 2^n bytes) receives
+ * PolarCode.frozen_mask, 1 = frozen -- exactly what
+ * pq_decoder_set_frozen_mask takes.  Host only, no device needed.         */
+int pq_read_code_table(const char *path, int *n, int *channel_tag, double *channel_param,
+                       double *target_fer, int *bins, uint8_t *mask_out, size_t mask_len);
+/* The table's checksum: BLAKE2b (RFC 7693), unkeyed, 8-byte digest, as a
+ * little-endian u64 (construction.py:458-459).                             */
+uint64_t pq_blake2b64(const void *data, size_t len);
+
 /* Copy the per-frame cycle profile of the last decode (PQ_OPT_PROFILE=1):
  * out[frame][PQ_PROF_SLOTS] = {upper f, upper g, upper other, shared f,
  * shared g, shared other, warp sub-trees, type staging, rate-1, total,

@@ -37,7 +37,7 @@ EXPORTS = (
     "pq_polar_transform", "pq_decoder_workspace_bytes", "pq_decoder_last_launches",
     "pq_decoder_destroy", "pq_last_error", "pq_abi_version", "pq_decoder_read_profile",
     "pq_debug_fmag", "pq_decoder_last_ctas_per_frame", "pq_decoder_last_config", "pq_sc_decode_q88",
-    "pq_decoder_kernel_times", "pq_hash_frames", "pq_verify_frames", "pq_xxh64", "pq_de_create", "pq_de_run", "pq_de_destroy",
+    "pq_decoder_kernel_times", "pq_read_code_table", "pq_blake2b64", "pq_hash_frames", "pq_verify_frames", "pq_xxh64", "pq_de_create", "pq_de_run", "pq_de_destroy",
 )
 
 _lib = None
@@ -75,6 +75,9 @@ def load():
     L.pq_decoder_destroy.argtypes = [vp]
     L.pq_decoder_read_profile.argtypes = [vp, vp, i]
     L.pq_decoder_kernel_times.argtypes = [vp, vp, i]
+    L.pq_read_code_table.argtypes = [ctypes.c_char_p, vp, vp, vp, vp, vp, vp, ctypes.c_size_t]
+    L.pq_blake2b64.argtypes = [ctypes.c_char_p, ctypes.c_size_t]
+    L.pq_blake2b64.restype = ctypes.c_uint64
     L.pq_debug_fmag.argtypes = [i, vp, vp, vp, i, vp]
     L.pq_hash_frames.argtypes = [u32p, i, i, ctypes.c_uint64, vp, vp]
     L.pq_verify_frames.argtypes = [u32p, i, i, ctypes.c_uint64, vp, vp, vp, vp]

@@ -12,7 +12,8 @@ import sys
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 SRC = os.path.join(HERE, "csrc", "polarsc.cu")
-SRCS = [SRC, os.path.join(HERE, "csrc", "verify.cu"), os.path.join(HERE, "csrc", "de.cu")]
+SRCS = [SRC, os.path.join(HERE, "csrc", "verify.cu"), os.path.join(HERE, "csrc", "de.cu"),
+        os.path.join(HERE, "csrc", "codetable.cu")]
 OUT = os.path.join(HERE, "libpolarsc.so")
 INCLUDE = os.path.join(os.path.dirname(HERE), "include")
 
@@ -35,7 +36,7 @@ def nvcc() -> str:
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
-    deps = [*SRCS, os.path.join(INCLUDE, "polarsc.h")]
+    deps = [*SRCS, os.path.join(INCLUDE, "polarsc.h"), os.path.join(HERE, "csrc", "serial_q88.cuh")]
     if not force and os.path.exists(OUT) and all(os.path.getmtime(OUT) >= os.path.getmtime(d) for d in deps):
         return OUT
     cmd = [nvcc(), *NVCC_FLAGS, "-o", OUT + ".tmp", *SRCS]

@@ -78,6 +78,33 @@ def write_code_table(code: PolarCode, path) -> None:
 
 
 def read_code_table(path) -> PolarCode:
+    """construction.py:483-507 through the C ABI (pq_read_code_table): the
+    same validation and ValueError messages as the reference."""
+    import ctypes
+
+    from . import _lib
+    L = _lib.load()
+    n, tag, bins = ctypes.c_int(), ctypes.c_int(), ctypes.c_int()
+    param, fer = ctypes.c_double(), ctypes.c_double()
+    bpath = os.fsencode(path)
+
+    def call(*args):
+        rc = L.pq_read_code_table(bpath, *args)
+        if rc == -2:
+            raise FileNotFoundError(L.pq_last_error().decode())
+        if rc < 0:
+            raise ValueError(L.pq_last_error().decode())  # the reference's messages
+        _lib.check(rc, "read_code_table")
+
+    call(ctypes.byref(n), ctypes.byref(tag), ctypes.byref(param), ctypes.byref(fer), ctypes.byref(bins), None, 0)
+    mask = np.zeros(1 << n.value, np.uint8)
+    call(None, None, None, None, None, mask.ctypes.data, mask.size)
+    return PolarCode(n=n.value, frozen_mask=mask, channel=channel_from_tag(tag.value, param.value),
+                     target_fer=fer.value, bins=bins.value)
+
+
+def read_code_table_py(path) -> PolarCode:
+    """Pure-Python restatement of the same reader (cross-check in tests)."""
     with open(path, "rb") as fh:
         blob = fh.read()
     hsz = struct.calcsize(_HEAD)
