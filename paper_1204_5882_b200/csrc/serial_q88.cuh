@@ -395,6 +395,95 @@ __device__ __forceinline__ uint32_t w32_body(int v, uint32_t m32)
     return (xl ^ xr) | (xr << 16);
 }
 
+// ---- widths 8..32 with a compile-time frozen pattern (SE_W32_SPEC): the whole
+// width-32 sub-tree as straight-line code.  SC's control flow does not depend
+// on the data, and density-evolution constructions draw their width-32
+// patterns from one small family (30 patterns cover every mixed width-32 node
+// of the BASELINE codes and of the Table-1 codes for n = 14..24), so each
+// pattern gets its own routine: no type tests, loops or calls inside, every
+// guard folded into one flag that is tested once at the end (a failed guard
+// re-decodes the sub-tree with the generic w32, which is decision-exact on
+// its own).  Lane-parallel at widths 32 and 16 (lane l = element l), rate-1
+// and repetition children of any width decided by ballot / redux without a
+// gather, mixed width-8 children gathered into the replicated routines.
+#ifndef SE_W32_SPEC
+#define SE_W32_SPEC 0  // measured: see the note at w32d
+#endif
+
+template <int W, uint32_t M>
+__device__ __forceinline__ uint32_t lnode(int v, bool &ok)
+{
+    constexpr int t = ntype(M, W);
+    const unsigned FULL = 0xffffffffu;
+    const int lane = threadIdx.x & 31;
+    if constexpr (t == T_R0) {
+        return 0u;
+    } else if constexpr (t == T_R1) {
+        ok &= __ballot_sync(FULL, (W == 32 || lane < W) && abs(v) < TAUI[clog2(W)]) == 0u;
+        return __ballot_sync(FULL, v < 0) & lm(W);
+    } else if constexpr (t == T_REP) {
+        // exact sum by redux when no pairwise partial sum can saturate
+        const int vv = (W == 32 || lane < W) ? v : 0;
+        const int tot = __reduce_add_sync(FULL, vv);
+        ok &= __reduce_add_sync(FULL, abs(vv)) <= 32767;
+        return tot < 0 ? lm(W) : 0u;
+    } else if constexpr (W == 8) {
+        int x[8];
+#pragma unroll
+        for (int i = 0; i < 8; i++) x[i] = __shfl_sync(FULL, v, i);
+        return rnode<8, M>(x, ok);
+    } else {
+        constexpr int H = W / 2;
+        constexpr uint32_t ML = M & lm(H), MR = M >> H;
+        const int b = __shfl_down_sync(FULL, v, H);  // lanes < H: the pair (l, l + H)
+        uint32_t xl = 0, xr = 0;
+        if constexpr (ntype(ML, H) != T_R0) xl = lnode<H, ML>(fq(v, b), ok);
+        if constexpr (ntype(MR, H) != T_R0) xr = lnode<H, MR>(gq(v, b, (xl >> lane) & 1u), ok);
+        return (xl ^ xr) | (xr << H);
+    }
+}
+
+__device__ __noinline__ uint32_t w32(int v, uint32_t m32);
+
+template <uint32_t M>
+__device__ __noinline__ uint32_t w32s(int v)
+{
+    bool ok = true;
+    const uint32_t r = lnode<32, M>(v, ok);
+    return ok ? r : w32(v, M);
+}
+
+// the width-32 patterns with a routine: X(mask), most frequent first
+#ifndef SE_W32_NPAT
+#define SE_W32_NPAT 2
+#endif
+#define SE_W32_P1(X) X(0x1u)
+#define SE_W32_P2(X) SE_W32_P1(X) X(0x10117u)
+#define SE_W32_P4(X) SE_W32_P2(X) X(0x177f7fffu) X(0x117177fu)
+#define SE_W32_P8(X) SE_W32_P4(X) X(0x117u) X(0x1011fu) X(0x177fffffu) X(0x17u)
+#define SE_W32_P12(X) SE_W32_P8(X) X(0x3u) X(0x11717ffu) X(0x7u) X(0x17ffffffu)
+#define SE_W32_P30(X)                                                                              \
+    SE_W32_P12(X) X(0x1013fu) X(0x77f7fffu) X(0x1171fffu)                                          \
+    X(0x7177fu) X(0x13f7fffu) X(0x37f7fffu) X(0x1fffffffu) X(0x17177fu) X(0x11f7fffu) X(0x1037fu)  \
+    X(0x17f7fffu) X(0x1017fu) X(0x1077fu) X(0x3177fu) X(0x1173fffu) X(0x3fffffffu) X(0x3077fu)    \
+    X(0x11f3fffu)
+#define SE_CAT_(a, b) a##b
+#define SE_CAT(a, b) SE_CAT_(a, b)
+#define SE_W32_PATTERNS(X) SE_CAT(SE_W32_P, SE_W32_NPAT)(X)
+
+__device__ __noinline__ uint32_t w32d(int v, uint32_t m32)
+{
+#if SE_W32_SPEC
+    switch (m32) {
+#define SE_X(mask) case mask: return w32s<mask>(v);
+        SE_W32_PATTERNS(SE_X)
+#undef SE_X
+    default: break;
+    }
+#endif
+    return w32(v, m32);
+}
+
 // ---- widths 64..512: lane l holds elements l + 32q (q < W/32) in registers
 // (in-lane f/g steps), the tree unrolled at compile time (node types as two
 // uniform masks, every type test a constant shift); the width-32 leaves are
@@ -423,7 +512,7 @@ __device__ __forceinline__ void wchild(const int (&x)[H / 32], const WalkCtx &c,
         constexpr int e = clog2(REL);
         const uint32_t pos = c.pos0 + 32u * (uint32_t)(REL - (1 << e));
         PQ_CHECK(e >= 0 && REL < 32);
-        xo[0] = w32(x[0], c.fm[pos >> 5]);
+        xo[0] = w32d(x[0], c.fm[pos >> 5]);
     } else {
         wnode<H, REL>(x, c, xo);
     }
@@ -1061,7 +1150,7 @@ __device__ __noinline__ void root(float *st_end, uint32_t *xs, const uint8_t *ty
 #endif
     } else {
         const uint32_t pos = (j0 * W) & (S - 1);
-        const uint32_t bits = w32(f2q((st_end - 64)[lane]), fm[pos >> 5]);
+        const uint32_t bits = w32d(f2q((st_end - 64)[lane]), fm[pos >> 5]);
         if (lane == 0) xs[pos >> 5] = bits;
         __syncwarp();
     }

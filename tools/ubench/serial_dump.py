@@ -1,11 +1,15 @@
-"""Real inputs of the single-warp band for serial_bench.cu.
+"""Real inputs of the single-warp band for tools/ubench/serial_bench.cu.
 
 Decodes frames of a BASELINE config with the fixed-point oracle (all-zero
 frozen values, so the textbook and the GPU's coset-shifted domains coincide),
 takes the stage dump, and writes every node the warp band is handed -- the
-visited non-rate-0 nodes of width WMAX (2048) -- in decode order: depth,
-index, its Q8.8 values and the expected partial-sum words T_W(u-hat of the
-node).  Output: tools/ubench/data/serial_<cfg>.bin (+ the frozen mask).
+visited non-rate-0 nodes of width WMAX (2048) -- in decode order.
+
+File (little endian): header int32 n, wl, frames, nodes; then per frame and
+node one record: int32 d0, uint32 j, int16 vals[W] (the node's Q8.8 LLRs),
+uint32 expect[W/32] (T_W(u-hat of the node)), uint8 ty[2W] (the node's local
+heap-order types, index (1 << e) + jj), uint32 fm[W/32] (frozen-mask words).
+Output: tools/ubench/data/serial_<cfg>.bin
 
 python tools/ubench/serial_dump.py [cfg=c3] [frames=2] [wmax_log2=11]
 """
@@ -35,11 +39,16 @@ W = 1 << wl
 d0 = n - wl
 ty = types(mask)
 vis = visited(ty)
-nodes = [j for j in np.nonzero(vis[d0])[0] if ty[d0][j] != 1]  # rate-0 nodes are zeroed by the block loop
+nodes = [int(j) for j in np.nonzero(vis[d0])[0] if ty[d0][j] != 1]  # rate-0 nodes are zeroed by the block loop
+local = {}
+for j in nodes:
+    t = np.zeros(2 * W, np.uint8)
+    for e in range(wl + 1):
+        t[(1 << e):(2 << e)] = ty[d0 + e][j << e:(j + 1) << e]
+    local[j] = t.tobytes() + pack_bits(mask[j * W:(j + 1) * W]).tobytes()
 rng = np.random.default_rng(77)
 out = bytearray()
 out += struct.pack("<iiii", n, wl, frames, len(nodes))
-out += pack_bits(mask).tobytes()
 for f in range(frames):
     u = (rng.random(N) < 0.5).astype(np.uint8) * (1 - mask)
     x = O.polar_transform_bytes(u)
@@ -57,6 +66,8 @@ for f in range(frames):
         out += struct.pack("<iI", d0, j)
         out += vals.tobytes()
         out += pack_bits(xw).tobytes()
+        out += local[j]
+os.makedirs(os.path.join(ROOT, "tools", "ubench", "data"), exist_ok=True)
 path = os.path.join(ROOT, "tools", "ubench", "data", f"serial_{key}.bin")
 open(path, "wb").write(out)
 print("->", path, len(out), "bytes")
