@@ -185,6 +185,21 @@ int pq_read_code_table(const char *path, int *n, int *channel_tag, double *chann
  * little-endian u64 (construction.py:458-459).                             */
 uint64_t pq_blake2b64(const void *data, size_t len);
 
+/* Seeded BSC trial inputs on the device (the frames of
+ * bench.run_trials).  Frame j0 + f reproduces the reference's
+ * numpy call sequence bit for bit (channel.py:66-73 make_rng, :116-125
+ * transmit):
+ *   x = make_rng(seed, 2j).integers(0, 2, N, dtype=uint8)
+ *   y = x ^ (make_rng(seed, 2j + 1).random(N) < p)
+ * packed LSB-first into x_words / y_words [frames][max(1, N/32)] (device).
+ * Stream-ordered.  pq_pcg64_seed is the host half: PCG64's (state, inc) after
+ * seeding from SeedSequence((seed, stream)), as {state_hi, state_lo, inc_hi,
+ * inc_lo} -- numpy's bit_generator.state.  BIAWGN noise is not generated on
+ * the device (see csrc/frames.cu).                                          */
+int pq_bsc_frames(int n, uint64_t seed, uint64_t j0, int frames, double p, uint32_t *x_words,
+                  uint32_t *y_words, void *stream);
+int pq_pcg64_seed(uint64_t seed, uint64_t stream, uint64_t out_state_inc[4]);
+
 /* Copy the per-frame cycle profile of the last decode (PQ_OPT_PROFILE=1):
  * out[frame][PQ_PROF_SLOTS] = {upper f, upper g, upper other, shared f,
  * shared g, shared other, warp sub-trees, type staging, rate-1, total,

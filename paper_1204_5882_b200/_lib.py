@@ -38,6 +38,7 @@ EXPORTS = (
     "pq_decoder_destroy", "pq_last_error", "pq_abi_version", "pq_decoder_read_profile",
     "pq_debug_fmag", "pq_decoder_last_ctas_per_frame", "pq_decoder_last_config", "pq_sc_decode_q88",
     "pq_decoder_kernel_times", "pq_read_code_table", "pq_blake2b64", "pq_hash_frames", "pq_verify_frames", "pq_xxh64", "pq_de_create", "pq_de_run", "pq_de_destroy",
+    "pq_bsc_frames", "pq_pcg64_seed",
 )
 
 _lib = None
@@ -87,6 +88,8 @@ def load():
     L.pq_de_create.argtypes = [ctypes.POINTER(vp), i, dbl, vp, vp, vp, vp, i]
     L.pq_de_run.argtypes = [vp, vp, i, dbl, dbl, dbl, vp]
     L.pq_de_destroy.argtypes = [vp]
+    L.pq_bsc_frames.argtypes = [i, ctypes.c_uint64, ctypes.c_uint64, i, dbl, u32p, u32p, vp]
+    L.pq_pcg64_seed.argtypes = [ctypes.c_uint64, ctypes.c_uint64, vp]
     L.pq_last_error.restype = ctypes.c_char_p
     L.pq_abi_version.restype = ctypes.c_int
     for name in EXPORTS:

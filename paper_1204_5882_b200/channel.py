@@ -150,3 +150,39 @@ def frames_batch(ch: ChannelModel, seed: int, j0: int, F: int, N: int, threads: 
         with ThreadPoolExecutor(max_workers=min(threads, F)) as ex:
             list(ex.map(one, range(F)))
     return x, llr, y_bits
+
+
+# --------------------------------------------------------------------------
+# the same frames on the device (csrc/frames.cu): BSC only -- numpy's bit and
+# uniform draws are integer arithmetic on the PCG64 stream and are reproduced
+# bit for bit; Generator.normal (BIAWGN) is not.
+
+def pcg64_seed(seed: int, stream: int) -> tuple[int, int]:
+    """(state, inc) of make_rng(seed, stream)'s PCG64 as the C library seeds
+    it (numpy: bit_generator.state["state"]); host only."""
+    import ctypes
+
+    from . import _lib
+    out = (ctypes.c_uint64 * 4)()
+    _lib.check(_lib.load().pq_pcg64_seed(seed, stream, out), "pq_pcg64_seed")
+    return (out[0] << 64) | out[1], (out[2] << 64) | out[3]
+
+
+def bsc_frames_device(ch: Bsc, seed: int, j0: int, F: int, n: int, device=None, stream=None):
+    """Frames j0 .. j0+F-1 of the seed convention above generated on the GPU:
+    (x_words, y_words), int32 CUDA tensors [F, max(1, 2^n / 32)], LSB-first --
+    identical to pack_bits of ``frame``'s outputs."""
+    import torch
+
+    from . import _lib
+    if not isinstance(ch, Bsc):
+        raise TypeError("device frame generation covers the BSC only (BIAWGN frames: frames_batch)")
+    dev = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
+    wpf = max(1, (1 << n) // 32)
+    s = torch.cuda.current_stream(dev) if stream is None else stream
+    with torch.cuda.device(dev), torch.cuda.stream(s):
+        xw = torch.empty((F, wpf), dtype=torch.int32, device=dev)
+        yw = torch.empty((F, wpf), dtype=torch.int32, device=dev)
+        _lib.check(_lib.load().pq_bsc_frames(n, seed, j0, F, float(ch.p), xw.data_ptr(), yw.data_ptr(),
+                                             s.cuda_stream), "pq_bsc_frames")
+    return xw, yw

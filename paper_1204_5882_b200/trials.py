@@ -9,7 +9,9 @@ run_trials(code, ch, trials, seed, representation) -> BenchRow
   SPEC.md:419).  Trial t uses make_rng(seed, 2t) for x and stream 2t+1 for the
   channel noise (the same frames whatever the batch size).
 
-Frames are decoded in batches on one GPU; verification compares x_hat with
+BSC frames are drawn on the device (the reference's numpy sequence, bit for
+bit: csrc/frames.cu); BIAWGN frames on host threads, one batch ahead of the
+decode.  Frames are decoded in batches on one GPU; verification compares x_hat with
 x on the device (equivalent to SPEC.md:318's hash check without the 2^-64
 collision term).  CSV output (``emit_csv``) follows SPEC.md:402-410.
 """
@@ -73,21 +75,25 @@ def run_trials(code: PolarCode, ch, trials: int, seed: int, representation: str 
     from concurrent.futures import ThreadPoolExecutor
 
     def host_batch(j0, F):
-        # threaded host generation of the next batch (channel.frames_batch),
+        # BIAWGN: threaded host generation of the next batch (channel.frames_batch),
         # overlapped with the device decode of the current one
-        x, llr, y = C.frames_batch(ch, seed, j0, F, N)
-        return x, (pack_bits(y) if is_bsc else llr)
+        x, llr, _ = C.frames_batch(ch, seed, j0, F, N, want_y=False)
+        return x, llr
 
-    gen = ThreadPoolExecutor(max_workers=1)
-    nxt = gen.submit(host_batch, 0, min(batch, trials))
+    gen = None if is_bsc else ThreadPoolExecutor(max_workers=1)
+    nxt = None if is_bsc else gen.submit(host_batch, 0, min(batch, trials))
     while done < trials:
         F = min(batch, trials - done)
-        x, inp = nxt.result()
-        if done + F < trials:
-            nxt = gen.submit(host_batch, done + F, min(batch, trials - done - F))
-        x_w = torch.from_numpy(pack_bits(x).view(np.int32).copy()).to(dev)
+        if is_bsc:
+            # BSC: the same numpy-seeded frames drawn on the device (csrc/frames.cu)
+            x_w, d_in = C.bsc_frames_device(ch, seed, done, F, n, device=dev)
+        else:
+            x, inp = nxt.result()
+            if done + F < trials:
+                nxt = gen.submit(host_batch, done + F, min(batch, trials - done - F))
+            x_w = torch.from_numpy(pack_bits(x).view(np.int32).copy()).to(dev)
+            d_in = torch.from_numpy(inp).to(dev)
         u_w = polar_transform_words(x_w, n)  # Alice's disclosure: u = T(x)
-        d_in = (torch.from_numpy(inp.view(np.int32).copy()) if is_bsc else torch.from_numpy(inp)).to(dev)
 
         def decode():
             if is_bsc:
@@ -106,7 +112,8 @@ def run_trials(code: PolarCode, ch, trials: int, seed: int, representation: str 
         decode_s += a.elapsed_time(b) / 1e3
         failures += int((x_hat[:F] != x_w).any(dim=1).sum().item())
         done += F
-    gen.shutdown()
+    if gen is not None:
+        gen.shutdown()
     wall = time.perf_counter() - t_wall
     return BenchRow(channel=_channel_name(ch), n=n, rate=code.rate, fer_measured=failures / trials,
                     trials=trials, throughput_mbps=trials * N / decode_s / 1e6, wall_time=wall, seed=seed,

@@ -6,4 +6,4 @@ set -e
 ROOT=$(cd "$(dirname "$0")/.." && pwd)
 mkdir -p "$ROOT/variants"
 nvcc -w -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 --fmad=false -prec-div=true -ftz=false -DPQ_ONLY_FIXED $EXTRA -I "$ROOT/include" \
-     -Xcompiler -fPIC -shared -cudart static -o "$ROOT/variants/$1.so" "$ROOT/paper_1204_5882_b200/csrc/polarsc.cu" "$ROOT/paper_1204_5882_b200/csrc/verify.cu" "$ROOT/paper_1204_5882_b200/csrc/de.cu" "$ROOT/paper_1204_5882_b200/csrc/codetable.cu"
+     -Xcompiler -fPIC -shared -cudart static -o "$ROOT/variants/$1.so" "$ROOT/paper_1204_5882_b200/csrc/polarsc.cu" "$ROOT/paper_1204_5882_b200/csrc/verify.cu" "$ROOT/paper_1204_5882_b200/csrc/de.cu" "$ROOT/paper_1204_5882_b200/csrc/codetable.cu" "$ROOT/paper_1204_5882_b200/csrc/frames.cu"
