@@ -1865,15 +1865,19 @@ __global__ void __launch_bounds__(NT, NT == 512 ? 1 : 2) sc_decode_kernel(DecPar
                 PROF_MARK(PR_TYPES);
                 // entering a shared-memory sub-tree: stage its node types
                 __syncthreads();
+                // the fixed-point serial engine reads node types down to the
+                // width-32 level only (below it the frozen-mask words): S / 16
+                // bytes instead of 2 S
+                const uint32_t qlim = se2 && S >= 32 ? S / 16 : 2 * S;
                 if (S >= 128) {
                     // levels e >= 4 are 16-byte aligned runs in both layouts: copy
                     // them as uint4 (4 loads per thread at S = 8192 instead of 64)
-                    if (tid < 15) {
+                    if (tid < 15 && 1 + tid < qlim) {
                         const uint32_t q = 1 + tid;
                         const int e = 31 - __clz(q);
                         sm.ty[q] = __ldg(p.types + ((size_t)1 << (dS + e)) + ((size_t)j << e) + (q - (1u << e)));
                     }
-                    for (uint32_t c = tid; c < (2 * S - 16) / 16; c += nthr) {
+                    for (uint32_t c = tid; 16 + 16 * c < qlim; c += nthr) {
                         const uint32_t q = 16 + 16 * c;
                         const int e = 31 - __clz(q);
                         const uint4 *src = reinterpret_cast<const uint4 *>(
@@ -1881,7 +1885,7 @@ __global__ void __launch_bounds__(NT, NT == 512 ? 1 : 2) sc_decode_kernel(DecPar
                         *reinterpret_cast<uint4 *>(sm.ty + q) = __ldg(src);
                     }
                 } else {
-                    for (uint32_t q = 1 + tid; q < 2 * S; q += nthr) {
+                    for (uint32_t q = 1 + tid; q < qlim; q += nthr) {
                         const int e = 31 - __clz(q);
                         sm.ty[q] = __ldg(p.types + ((size_t)1 << (dS + e)) + ((size_t)j << e) + (q - (1u << e)));
                     }
