@@ -42,12 +42,6 @@
 #ifndef SE_UNR
 #define SE_UNR 256  // widest node of the compile-time unrolled register walk
 #endif
-#ifndef SE_TREE
-#define SE_TREE 0
-#endif
-#ifndef SE_WIDE_COMPACT
-#define SE_WIDE_COMPACT 0
-#endif
 #ifndef SE_SPEC_LP
 #define SE_SPEC_LP 0
 #endif
@@ -395,20 +389,26 @@ __device__ __forceinline__ uint32_t w32_body(int v, uint32_t m32)
     return (xl ^ xr) | (xr << 16);
 }
 
-// ---- widths 8..32 with a compile-time frozen pattern (SE_W32_SPEC): the whole
-// width-32 sub-tree as straight-line code.  SC's control flow does not depend
-// on the data, and density-evolution constructions draw their width-32
-// patterns from one small family (30 patterns cover every mixed width-32 node
-// of the BASELINE codes and of the Table-1 codes for n = 14..24), so each
-// pattern gets its own routine: no type tests, loops or calls inside, every
-// guard folded into one flag that is tested once at the end (a failed guard
+// ---- widths 8..32 with a compile-time frozen pattern: a whole width-32
+// sub-tree as straight-line code.  SC's control flow does not depend on the
+// data, and density-evolution constructions draw their width-32 patterns from
+// one small family (30 patterns cover every mixed width-32 node of the
+// BASELINE codes and of the Table-1 codes for n = 14..24), so a pattern can
+// have its own routine: no type tests, loops or calls inside, every guard
+// folded into one flag that is tested once at the end (a failed guard
 // re-decodes the sub-tree with the generic w32, which is decision-exact on
 // its own).  Lane-parallel at widths 32 and 16 (lane l = element l), rate-1
 // and repetition children of any width decided by ballot / redux without a
 // gather, mixed width-8 children gathered into the replicated routines.
-#ifndef SE_W32_SPEC
-#define SE_W32_SPEC 0  // measured: see the note at w32d
-#endif
+// A routine executes ~40 % fewer instructions than the generic w32 on the same
+// node, but every routine is 8-19 KB of code that runs once per call, so the
+// gain is bounded by instruction fetch: with all 30 patterns the serial warp
+// stalls 32 % of its cycles on fetch and c3 (two CTAs per SM) loses 21 %.  The
+// engine is therefore templated on SP: the routines of the SE_W32_NPAT most
+// frequent patterns (2: F I^31 and 0x10117, 43 % of c3's mixed width-32
+// nodes) are compiled into the clustered kernels only (one CTA per SM: c5
+// +4.6 %); with two CTAs per SM the same two routines cost c3 1 %, so those
+// kernels keep SP = false (profiles/r02/ab_w32_patterns.txt).
 
 template <int W, uint32_t M>
 __device__ __forceinline__ uint32_t lnode(int v, bool &ok)
@@ -471,16 +471,14 @@ __device__ __noinline__ uint32_t w32s(int v)
 #define SE_CAT(a, b) SE_CAT_(a, b)
 #define SE_W32_PATTERNS(X) SE_CAT(SE_W32_P, SE_W32_NPAT)(X)
 
-__device__ __noinline__ uint32_t w32d(int v, uint32_t m32)
+template <bool SP>
+__device__ __forceinline__ uint32_t w32d(int v, uint32_t m32)
 {
-#if SE_W32_SPEC
-    switch (m32) {
-#define SE_X(mask) case mask: return w32s<mask>(v);
+    if constexpr (SP) {
+#define SE_X(mask) if (m32 == mask) return w32s<mask>(v);
         SE_W32_PATTERNS(SE_X)
 #undef SE_X
-    default: break;
     }
-#endif
     return w32(v, m32);
 }
 
@@ -501,10 +499,10 @@ __device__ __forceinline__ int wtype(const WalkCtx &c)
     return (int)(((c.wb0 >> REL) & 1u) | (((c.wb1 >> REL) & 1u) << 1));
 }
 
-template <int W, int REL>
+template <int W, int REL, bool SP>
 __device__ __forceinline__ void wnode(const int (&x)[W / 32], const WalkCtx &c, uint32_t (&xo)[W / 32]);
 
-template <int H, int REL>
+template <int H, int REL, bool SP>
 __device__ __forceinline__ void wchild(const int (&x)[H / 32], const WalkCtx &c, uint32_t (&xo)[H / 32])
 {
     if constexpr (H == 32) {
@@ -512,13 +510,13 @@ __device__ __forceinline__ void wchild(const int (&x)[H / 32], const WalkCtx &c,
         constexpr int e = clog2(REL);
         const uint32_t pos = c.pos0 + 32u * (uint32_t)(REL - (1 << e));
         PQ_CHECK(e >= 0 && REL < 32);
-        xo[0] = w32d(x[0], c.fm[pos >> 5]);
+        xo[0] = w32d<SP>(x[0], c.fm[pos >> 5]);
     } else {
-        wnode<H, REL>(x, c, xo);
+        wnode<H, REL, SP>(x, c, xo);
     }
 }
 
-template <int W, int REL>
+template <int W, int REL, bool SP>
 __device__ __forceinline__ void wnode(const int (&x)[W / 32], const WalkCtx &c, uint32_t (&xo)[W / 32])
 {
     constexpr int V = W / 32, Vh = V / 2;
@@ -573,7 +571,7 @@ __device__ __forceinline__ void wnode(const int (&x)[W / 32], const WalkCtx &c, 
     } else {
 #pragma unroll
         for (int q = 0; q < Vh; q++) ch[q] = fq(x[q], x[q + Vh]);
-        wchild<W / 2, 2 * REL>(ch, c, xl);
+        wchild<W / 2, 2 * REL, SP>(ch, c, xl);
     }
     if (wtype<2 * REL + 1>(c) == T_R0) {
 #pragma unroll
@@ -581,7 +579,7 @@ __device__ __forceinline__ void wnode(const int (&x)[W / 32], const WalkCtx &c, 
     } else {
 #pragma unroll
         for (int q = 0; q < Vh; q++) ch[q] = gq(x[q], x[q + Vh], (xl[q] >> lane) & 1u);
-        wchild<W / 2, 2 * REL + 1>(ch, c, xr);
+        wchild<W / 2, 2 * REL + 1, SP>(ch, c, xr);
     }
 #pragma unroll
     for (int q = 0; q < Vh; q++) {
@@ -601,7 +599,7 @@ __device__ __forceinline__ void put_words(uint32_t *xw, const uint32_t (&xo)[V])
     if (lane < V) xw[lane] = w;
 }
 
-template <int W>
+template <int W, bool SP>
 __device__ __forceinline__ void walk_root(const int *nd, uint32_t *xw, const WalkCtx &c)
 {
     constexpr int V = W / 32;
@@ -610,11 +608,12 @@ __device__ __forceinline__ void walk_root(const int *nd, uint32_t *xw, const Wal
     uint32_t xo[V];
 #pragma unroll
     for (int q = 0; q < V; q++) x[q] = nd[32 * q + lane];
-    wnode<W, 1>(x, c, xo);
+    wnode<W, 1, SP>(x, c, xo);
     put_words<V>(xw, xo);
 }
 
 // the walk from a width-W (64..512) node whose int values are at nd
+template <bool SP>
 __device__ __noinline__ void walk(const int *nd, uint32_t *xs, const uint8_t *ty, const uint32_t *fm, uint32_t S,
                                   int dS, int d0, uint32_t j0)
 {
@@ -637,15 +636,15 @@ __device__ __noinline__ void walk(const int *nd, uint32_t *xs, const uint8_t *ty
     uint32_t *xw = xs + (c.pos0 >> 5);
     SE_T0();
 #if SE_UNR >= 512
-    if (W == 512) walk_root<512>(nd, xw, c);
+    if (W == 512) walk_root<512, SP>(nd, xw, c);
     else
 #endif
 #if SE_UNR >= 256
-    if (W == 256) walk_root<256>(nd, xw, c);
+    if (W == 256) walk_root<256, SP>(nd, xw, c);
     else
 #endif
-    if (W == 128) walk_root<128>(nd, xw, c);
-    else walk_root<64>(nd, xw, c);
+    if (W == 128) walk_root<128, SP>(nd, xw, c);
+    else walk_root<64, SP>(nd, xw, c);
     SE_T1(3);
 }
 
@@ -658,7 +657,7 @@ __device__ __noinline__ void walk(const int *nd, uint32_t *xs, const uint8_t *ty
 // per lane before it computes or stores (the stage buffers are one shared
 // array: without the batching each element's loads would wait for the
 // previous element's store).
-template <int W, bool FROM_F32>
+template <int W, bool FROM_F32, bool SP>
 __device__ __forceinline__ void wide(float *st_end, uint32_t *xs, const uint8_t *ty, const uint32_t *fm, uint32_t S,
                                      int dS, int d0, uint32_t j0)
 {
@@ -762,8 +761,8 @@ __device__ __forceinline__ void wide(float *st_end, uint32_t *xs, const uint8_t 
             for (int k = 0; k < B; k++) ch[32 * (q0 + k) + lane] = fq(a[k], b[k]);
         }
         __syncwarp();
-        if constexpr (W / 2 > SE_UNR) wide<W / 2, false>(st_end, xs, ty, fm, S, dS, d0 + 1, 2 * j0);
-        else walk(reinterpret_cast<const int *>(st_end - W), xs, ty, fm, S, dS, d0 + 1, 2 * j0);
+        if constexpr (W / 2 > SE_UNR) wide<W / 2, false, SP>(st_end, xs, ty, fm, S, dS, d0 + 1, 2 * j0);
+        else walk<SP>(reinterpret_cast<const int *>(st_end - W), xs, ty, fm, S, dS, d0 + 1, 2 * j0);
     }
     if (tr == T_R0) {
         for (int q = lane; q < Vh; q += 32) xw[Vh + q] = 0u;
@@ -783,271 +782,18 @@ __device__ __forceinline__ void wide(float *st_end, uint32_t *xs, const uint8_t 
             for (int k = 0; k < B; k++) ch[32 * (q0 + k) + lane] = gq(a[k], b[k], (sw[k] >> lane) & 1u);
         }
         __syncwarp();
-        if constexpr (W / 2 > SE_UNR) wide<W / 2, false>(st_end, xs, ty, fm, S, dS, d0 + 1, 2 * j0 + 1);
-        else walk(reinterpret_cast<const int *>(st_end - W), xs, ty, fm, S, dS, d0 + 1, 2 * j0 + 1);
+        if constexpr (W / 2 > SE_UNR) wide<W / 2, false, SP>(st_end, xs, ty, fm, S, dS, d0 + 1, 2 * j0 + 1);
+        else walk<SP>(reinterpret_cast<const int *>(st_end - W), xs, ty, fm, S, dS, d0 + 1, 2 * j0 + 1);
     }
     for (int q = lane; q < Vh; q += 32) xw[q] ^= xw[Vh + q];
     __syncwarp();
-}
-
-// compact variant of wide (SE_WIDE_COMPACT): one out-of-line copy per width,
-// the two children through one loop body, the node already int.  Smaller
-// code: the band is re-entered ~300 times per N = 2^20 frame after block and
-// upper-band steps have evicted its instructions from the SM's caches.
-template <int W>
-__device__ __noinline__ void widec(float *st_end, uint32_t *xs, const uint8_t *ty, const uint32_t *fm, uint32_t S,
-                                   int dS, int d0, uint32_t j0)
-{
-    constexpr int V = W / 32, Vh = V / 2, B = 8;
-    const unsigned FULL = 0xffffffffu;
-    const int lane = threadIdx.x & 31;
-    const int e = d0 - dS;
-    const uint32_t lh = (1u << e) + (j0 & ((1u << e) - 1u));
-    const int *nd = reinterpret_cast<const int *>(st_end - 2 * W);
-    int *ch = reinterpret_cast<int *>(st_end - W);
-    uint32_t *xw = xs + (((j0 * W) & (S - 1)) >> 5);
-    const uint8_t t = ty[lh];
-    if (t == T_R0) {
-        for (int q = lane; q < V; q += 32) xw[q] = 0u;
-        __syncwarp();
-        return;
-    }
-    if (t == T_R1) {
-        int mn = 0x7fffffff;
-#pragma unroll 1
-        for (int q0 = 0; q0 < V; q0 += B) {
-            int a[B];
-#pragma unroll
-            for (int k = 0; k < B; k++) a[k] = nd[32 * (q0 + k) + lane];
-#pragma unroll
-            for (int k = 0; k < B; k++) mn = min(mn, abs(a[k]));
-        }
-        if (__all_sync(FULL, mn >= TAUI[clog2(W)])) {
-#pragma unroll 1
-            for (int q0 = 0; q0 < V; q0 += B) {
-                int a[B];
-#pragma unroll
-                for (int k = 0; k < B; k++) a[k] = nd[32 * (q0 + k) + lane];
-                uint32_t w = 0;
-#pragma unroll
-                for (int k = 0; k < B; k++) {
-                    const uint32_t b = __ballot_sync(FULL, a[k] < 0);
-                    w = lane == k ? b : w;
-                }
-                if (lane < B) xw[q0 + lane] = w;
-            }
-            __syncwarp();
-            return;
-        }
-    }
-    if (t == T_REP) {
-        // SC's pairing order: fold the in-lane levels through the free child
-        // area, then the lanes
-#pragma unroll 1
-        for (int hv = V / 2; hv >= 1; hv >>= 1)
-#pragma unroll 1
-            for (int q = 0; q < hv; q++) {
-                const int a = hv == V / 2 ? nd[32 * q + lane] : ch[32 * q + lane];
-                const int b = hv == V / 2 ? nd[32 * (q + hv) + lane] : ch[32 * (q + hv) + lane];
-                __syncwarp();
-                ch[32 * q + lane] = qa(b, a);
-                __syncwarp();
-            }
-        int s0 = ch[lane];
-#pragma unroll
-        for (int hh = 16; hh >= 1; hh >>= 1) s0 = qa(__shfl_down_sync(FULL, s0, hh), s0);
-        const uint32_t bits = __shfl_sync(FULL, s0, 0) < 0 ? FULL : 0u;
-        for (int q = lane; q < V; q += 32) xw[q] = bits;
-        __syncwarp();
-        return;
-    }
-#pragma unroll 1
-    for (int side = 0; side < 2; side++) {
-        if (ty[2 * lh + side] == T_R0) {
-            for (int q = lane; q < Vh; q += 32) xw[side * Vh + q] = 0u;
-            __syncwarp();
-            continue;
-        }
-#pragma unroll 1
-        for (int q0 = 0; q0 < Vh; q0 += B) {
-            int a[B], b[B];
-            uint32_t sw[B];
-#pragma unroll
-            for (int k = 0; k < B; k++) {
-                a[k] = nd[32 * (q0 + k) + lane];
-                b[k] = nd[32 * (q0 + k) + lane + W / 2];
-                sw[k] = side ? xw[q0 + k] : 0u;
-            }
-            if (side) {
-#pragma unroll
-                for (int k = 0; k < B; k++) ch[32 * (q0 + k) + lane] = gq(a[k], b[k], (sw[k] >> lane) & 1u);
-            } else {
-#pragma unroll
-                for (int k = 0; k < B; k++) ch[32 * (q0 + k) + lane] = fq(a[k], b[k]);
-            }
-        }
-        __syncwarp();
-        if constexpr (W / 2 > SE_UNR) widec<W / 2>(st_end, xs, ty, fm, S, dS, d0 + 1, 2 * j0 + side);
-        else walk(reinterpret_cast<const int *>(st_end - W), xs, ty, fm, S, dS, d0 + 1, 2 * j0 + side);
-    }
-    for (int q = lane; q < Vh; q += 32) xw[q] ^= xw[Vh + q];
-    __syncwarp();
-}
-
-// ---- widths above SE_UNR, iterative form (SE_TREE): a walk over the
-// shared-memory stage buffers (node of width W at st_end - 2W, int codes) with
-// one copy of each step for every width -- no per-position copies and no
-// calls per node (the band is re-entered ~300 times per 2^20 frame after
-// block and upper-band steps have evicted its instructions).  Every loop
-// loads a batch before it computes or stores (one shared array: unbatched,
-// each element's loads would wait for the previous element's store).
-__device__ __noinline__ void tree(float *st_end, uint32_t *xs, const uint8_t *ty, const uint32_t *fm, uint32_t S,
-                                  int dS, int d0, uint32_t j0)
-{
-    constexpr int B = 8;
-    const unsigned FULL = 0xffffffffu;
-    const int lane = threadIdx.x & 31;
-    int d = d0;
-    uint32_t j = j0;
-    bool entering = true;
-    for (;;) {
-        const uint32_t W = S >> (d - dS);
-        const int V = (int)(W >> 5), lgW = 31 - __clz(W);
-        const int e = d - dS;
-        const uint32_t lh = (1u << e) + (j & ((1u << e) - 1u));
-        int *nd = reinterpret_cast<int *>(st_end - 2 * W);
-        uint32_t *xw = xs + (((j * W) & (S - 1)) >> 5);
-        if (entering) {
-            entering = false;
-            if (W <= SE_UNR) {
-                walk(nd, xs, ty, fm, S, dS, d, j);
-                continue;
-            }
-            const uint8_t t = ty[lh];
-            if (t == T_R0) {
-                for (int q = lane; q < V; q += 32) xw[q] = 0u;
-                __syncwarp();
-                continue;
-            }
-            if (t == T_R1) {
-                int mn = 0x7fffffff;
-#pragma unroll 1
-                for (int q0 = 0; q0 < V; q0 += B) {
-                    int a[B];
-#pragma unroll
-                    for (int k = 0; k < B; k++) a[k] = q0 + k < V ? nd[32 * (q0 + k) + lane] : 0x7fffffff;
-#pragma unroll
-                    for (int k = 0; k < B; k++) mn = min(mn, abs(a[k]));
-                }
-                if (__all_sync(FULL, mn >= TAUI[lgW])) {
-#pragma unroll 1
-                    for (int q0 = 0; q0 < V; q0 += B) {
-                        int a[B];
-#pragma unroll
-                        for (int k = 0; k < B; k++) a[k] = q0 + k < V ? nd[32 * (q0 + k) + lane] : 0;
-                        uint32_t w = 0;
-#pragma unroll
-                        for (int k = 0; k < B; k++) {
-                            const uint32_t b = __ballot_sync(FULL, a[k] < 0);
-                            w = lane == k ? b : w;
-                        }
-                        if (lane < B && q0 + lane < V) xw[q0 + lane] = w;
-                    }
-                    __syncwarp();
-                    continue;
-                }
-            }
-            if (t == T_REP) {
-                // SC's pairing order: fold the in-lane levels through the free
-                // child area, then the lanes
-                int *tmp = reinterpret_cast<int *>(st_end - W);
-#pragma unroll 1
-                for (int hv = V / 2; hv >= 1; hv >>= 1)
-#pragma unroll 1
-                    for (int q = 0; q < hv; q++) {
-                        const int *src = hv == V / 2 ? nd : tmp;
-                        const int a = src[32 * q + lane], b = src[32 * (q + hv) + lane];
-                        __syncwarp();
-                        tmp[32 * q + lane] = qa(b, a);
-                        __syncwarp();
-                    }
-                int acc = tmp[lane];
-#pragma unroll
-                for (int hh = 16; hh >= 1; hh >>= 1) acc = qa(__shfl_down_sync(FULL, acc, hh), acc);
-                const uint32_t bits = __shfl_sync(FULL, acc, 0) < 0 ? FULL : 0u;
-                for (int q = lane; q < V; q += 32) xw[q] = bits;
-                __syncwarp();
-                continue;
-            }
-            // mixed (or a rate-1 node whose guard failed): f-step into the left child
-            d++;
-            j = 2 * j;
-            if (ty[2 * lh] == T_R0) {
-                for (int q = lane; q < V / 2; q += 32) xw[q] = 0u;
-                __syncwarp();
-                continue;  // the left child is decided
-            }
-            int *ch = reinterpret_cast<int *>(st_end - W);
-            const int Vh = V / 2;
-#pragma unroll 1
-            for (int q0 = 0; q0 < Vh; q0 += B) {
-                int a[B], b[B];
-#pragma unroll
-                for (int k = 0; k < B; k++) {
-                    a[k] = nd[32 * (q0 + k) + lane];
-                    b[k] = nd[32 * (q0 + k) + lane + W / 2];
-                }
-#pragma unroll
-                for (int k = 0; k < B; k++)
-                    if (q0 + k < Vh) ch[32 * (q0 + k) + lane] = fq(a[k], b[k]);
-            }
-            __syncwarp();
-            entering = true;
-            continue;
-        }
-        // ---- node (d, j) is decided
-        if (d == d0) break;
-        if ((j & 1u) == 0) {
-            // left child done -> g-step at the parent into the right child
-            j = j + 1;
-            uint32_t *xr = xw + V;
-            if (ty[lh + 1] == T_R0) {
-                for (int q = lane; q < V; q += 32) xr[q] = 0u;
-                __syncwarp();
-                continue;  // the right child is decided
-            }
-            const int *pa = reinterpret_cast<const int *>(st_end - 4 * W);  // the parent (width 2W)
-#pragma unroll 1
-            for (int q0 = 0; q0 < V; q0 += B) {
-                int a[B], b[B];
-                uint32_t sw[B];
-#pragma unroll
-                for (int k = 0; k < B; k++) {
-                    a[k] = pa[32 * (q0 + k) + lane];
-                    b[k] = pa[32 * (q0 + k) + lane + W];
-                    sw[k] = xw[q0 + k];
-                }
-#pragma unroll
-                for (int k = 0; k < B; k++)
-                    if (q0 + k < V) nd[32 * (q0 + k) + lane] = gq(a[k], b[k], (sw[k] >> lane) & 1u);
-            }
-            __syncwarp();
-            entering = true;
-            continue;
-        }
-        // right child done -> the parent's partial sums (xl ^ xr, xr)
-        uint32_t *xl = xw - V;
-        for (int q = lane; q < V; q += 32) xl[q] ^= xw[q];
-        __syncwarp();
-        d--;
-        j >>= 1;
-    }
 }
 
 // Entry: the node (d0, j0) of width W = S >> (d0 - dS), 32 <= W <= 2048, whose
 // fp32 Q8.8 values are in the shared stage buffer at st_end - 2W; writes its
 // partial-sum words to xs (S-local).  ty: S-local heap types; fm: the
 // S-sub-tree's frozen-mask words.  One warp.
+template <bool SP>
 __device__ __noinline__ void root(float *st_end, uint32_t *xs, const uint8_t *ty, const uint32_t *fm, uint32_t S,
                                   int dS, int d0, uint32_t j0)
 {
@@ -1055,83 +801,30 @@ __device__ __noinline__ void root(float *st_end, uint32_t *xs, const uint8_t *ty
     const uint32_t W = S >> (d0 - dS);
     PQ_CHECK(W >= 32 && W <= S && d0 >= dS && ((j0 * W) & (S - 1)) + W <= S);
     PQ_JITTER();
-#if SE_TREE
-    if (W >= 64) {
-        // the node's fp32 codes -> int in place (batched: loads ahead of stores)
-        float *nd = st_end - 2 * W;
-#pragma unroll 1
-        for (uint32_t i0 = 0; i0 < W; i0 += 256) {
-            float a[8];
-#pragma unroll
-            for (int k = 0; k < 8; k++) a[k] = i0 + 32 * k < W ? nd[i0 + 32 * k + lane] : 0.0f;
-#pragma unroll
-            for (int k = 0; k < 8; k++)
-                if (i0 + 32 * k < W) reinterpret_cast<int *>(nd)[i0 + 32 * k + lane] = f2q(a[k]);
-        }
-        __syncwarp();
-        if (W > SE_UNR) tree(st_end, xs, ty, fm, S, dS, d0, j0);
-        else walk(reinterpret_cast<const int *>(nd), xs, ty, fm, S, dS, d0, j0);
-#elif SE_WIDE_COMPACT
-    if (W >= 64) {
-        // the node's fp32 codes -> int in place (batched: loads ahead of stores)
-        float *nd = st_end - 2 * W;
-#pragma unroll 1
-        for (uint32_t i0 = 0; i0 < W; i0 += 256) {
-            float a[8];
-#pragma unroll
-            for (int k = 0; k < 8; k++) a[k] = i0 + 32 * k < W ? nd[i0 + 32 * k + lane] : 0.0f;
-#pragma unroll
-            for (int k = 0; k < 8; k++)
-                if (i0 + 32 * k < W) reinterpret_cast<int *>(nd)[i0 + 32 * k + lane] = f2q(a[k]);
-        }
-        __syncwarp();
-        if (W > SE_UNR) {
-            if (false) {
-#if PQ_WIDE_WARP_LOG2 >= 12
-            } else if (W == 4096) {
-                widec<4096>(st_end, xs, ty, fm, S, dS, d0, j0);
-#endif
-            } else if (W == 2048) {
-                widec<2048>(st_end, xs, ty, fm, S, dS, d0, j0);
-            } else if (W == 1024) {
-                widec<1024>(st_end, xs, ty, fm, S, dS, d0, j0);
-#if SE_UNR < 512
-            } else if (W == 512) {
-                widec<512>(st_end, xs, ty, fm, S, dS, d0, j0);
-#endif
-#if SE_UNR < 256
-            } else {
-                widec<256>(st_end, xs, ty, fm, S, dS, d0, j0);
-#endif
-            }
-        } else {
-            walk(reinterpret_cast<const int *>(nd), xs, ty, fm, S, dS, d0, j0);
-        }
-#else
     if (false) {
 #if PQ_WIDE_WARP_LOG2 >= 14
     } else if (W == 16384) {
-        wide<16384, true>(st_end, xs, ty, fm, S, dS, d0, j0);
+        wide<16384, true, SP>(st_end, xs, ty, fm, S, dS, d0, j0);
 #endif
 #if PQ_WIDE_WARP_LOG2 >= 13
     } else if (W == 8192) {
-        wide<8192, true>(st_end, xs, ty, fm, S, dS, d0, j0);
+        wide<8192, true, SP>(st_end, xs, ty, fm, S, dS, d0, j0);
 #endif
 #if PQ_WIDE_WARP_LOG2 >= 12
     } else if (W == 4096) {
-        wide<4096, true>(st_end, xs, ty, fm, S, dS, d0, j0);
+        wide<4096, true, SP>(st_end, xs, ty, fm, S, dS, d0, j0);
 #endif
     } else if (W == 2048) {
-        wide<2048, true>(st_end, xs, ty, fm, S, dS, d0, j0);
+        wide<2048, true, SP>(st_end, xs, ty, fm, S, dS, d0, j0);
     } else if (W == 1024) {
-        wide<1024, true>(st_end, xs, ty, fm, S, dS, d0, j0);
+        wide<1024, true, SP>(st_end, xs, ty, fm, S, dS, d0, j0);
 #if SE_UNR < 512
     } else if (W == 512) {
-        wide<512, true>(st_end, xs, ty, fm, S, dS, d0, j0);
+        wide<512, true, SP>(st_end, xs, ty, fm, S, dS, d0, j0);
 #endif
 #if SE_UNR < 256
     } else if (W == 256) {
-        wide<256, true>(st_end, xs, ty, fm, S, dS, d0, j0);
+        wide<256, true, SP>(st_end, xs, ty, fm, S, dS, d0, j0);
 #endif
     } else if (W >= 64) {
         // the node's fp32 codes -> int in place (batched: loads ahead of stores)
@@ -1146,11 +839,10 @@ __device__ __noinline__ void root(float *st_end, uint32_t *xs, const uint8_t *ty
                 if (i0 + 32 * k < W) reinterpret_cast<int *>(nd)[i0 + 32 * k + lane] = f2q(a[k]);
         }
         __syncwarp();
-        walk(reinterpret_cast<const int *>(nd), xs, ty, fm, S, dS, d0, j0);
-#endif
+        walk<SP>(reinterpret_cast<const int *>(nd), xs, ty, fm, S, dS, d0, j0);
     } else {
         const uint32_t pos = (j0 * W) & (S - 1);
-        const uint32_t bits = w32d(f2q((st_end - 64)[lane]), fm[pos >> 5]);
+        const uint32_t bits = w32d<SP>(f2q((st_end - 64)[lane]), fm[pos >> 5]);
         if (lane == 0) xs[pos >> 5] = bits;
         __syncwarp();
     }

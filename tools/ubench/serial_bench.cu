@@ -6,7 +6,7 @@
 // block, so that engine variants can be compared without the rest of the kernel.
 //
 // build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 \
-//          [-DSE_PROF] [-DSE_HEADER='"other.cuh"'] [-D...] -o serial_bench serial_bench.cu
+//          [-DSE_PROF] [-DSE_SP=true] [-DSE_W32_NPAT=n] [-D...] -o serial_bench serial_bench.cu
 // run:   serial_bench data/serial_c3.bin [blocks=296] [threads=256] [reps=3]
 #include <cuda_runtime.h>
 #include <limits.h>
@@ -25,6 +25,9 @@
 #define PQ_WIDE_WARP_LOG2 11
 #endif
 __constant__ float CORR_TAB_C[4097];
+#ifndef SE_SP
+#define SE_SP false  // true: the pattern routines of the clustered kernels
+#endif
 #ifndef SE_HEADER
 #define SE_HEADER "../../paper_1204_5882_b200/csrc/serial_q88.cuh"
 #endif
@@ -90,7 +93,7 @@ replay(const Rec *recs, int nodes, int frames, int wl, unsigned long long *cycle
         __syncthreads();
         if (tid < 32) {
             const long long t0 = clock64();
-            se::root(st + 2 * S, xs, ty, fm, S, r.d0, r.d0, r.j);
+            se::root<SE_SP>(st + 2 * S, xs, ty, fm, S, r.d0, r.d0, r.j);
             total += clock64() - t0;
         } else if (ICF_REPS) {
             for (int q = 0; q < ICF_REPS; q++) fl = icache_filler(fl);
