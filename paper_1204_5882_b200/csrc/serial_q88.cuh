@@ -45,6 +45,10 @@
 #ifndef SE_SPEC_LP
 #define SE_SPEC_LP 0
 #endif
+#ifndef SE_UNIFORM_MASK
+#define SE_UNIFORM_MASK 1
+#endif
+
 
 namespace se {
 
@@ -334,6 +338,20 @@ __device__ __forceinline__ uint32_t w32_body(int v, uint32_t m32);
 __device__ __noinline__ uint32_t w32(int v, uint32_t m32)
 {
     SE_T0();
+#if SE_UNIFORM_MASK
+    // The mask is warp-uniform, but as the argument of an out-of-line function
+    // the compiler must treat it as divergent: every type test below became a
+    // potentially divergent branch with a convergence barrier (BSSY / BSYNC /
+    // BREAK) and every shuffle or vote a divergence check (BRA.DIV, WARPSYNC).
+    // One redux hands it back as a uniform register: the branches on it are
+    // uniform branches and the barriers and checks disappear (w32: 809 -> 555
+    // SASS instructions, none of them BSSY).  c2..c5 +4.6 .. +7.3 %.  The same
+    // trick on the width-8 fallback, the wide levels' types, the register
+    // walk's type masks or per node costs 3-5 % (profiles/r02/ab_uniform.txt):
+    // there the uniform value turns selects into branches or sits on the
+    // address path.
+    m32 = __reduce_or_sync(0xffffffffu, m32);
+#endif
     const uint32_t r = w32_body(v, m32);
     SE_T1(2);
     return r;
@@ -522,7 +540,7 @@ __device__ __forceinline__ void wnode(const int (&x)[W / 32], const WalkCtx &c, 
     constexpr int V = W / 32, Vh = V / 2;
     const unsigned FULL = 0xffffffffu;
     const int lane = threadIdx.x & 31;
-    const int t = wtype<REL>(c);
+    const int t = wtype<REL>(c), tl = wtype<2 * REL>(c), tr = wtype<2 * REL + 1>(c);
     if (t == T_R0) {
 #pragma unroll
         for (int q = 0; q < V; q++) xo[q] = 0u;
@@ -565,7 +583,7 @@ __device__ __forceinline__ void wnode(const int (&x)[W / 32], const WalkCtx &c, 
     // their own guards, exactly as in polarsc.cu)
     int ch[Vh];
     uint32_t xl[Vh], xr[Vh];
-    if (wtype<2 * REL>(c) == T_R0) {
+    if (tl == T_R0) {
 #pragma unroll
         for (int q = 0; q < Vh; q++) xl[q] = 0u;
     } else {
@@ -573,7 +591,7 @@ __device__ __forceinline__ void wnode(const int (&x)[W / 32], const WalkCtx &c, 
         for (int q = 0; q < Vh; q++) ch[q] = fq(x[q], x[q + Vh]);
         wchild<W / 2, 2 * REL, SP>(ch, c, xl);
     }
-    if (wtype<2 * REL + 1>(c) == T_R0) {
+    if (tr == T_R0) {
 #pragma unroll
         for (int q = 0; q < Vh; q++) xr[q] = 0u;
     } else {
@@ -793,8 +811,16 @@ __device__ __forceinline__ void wide(float *st_end, uint32_t *xs, const uint8_t 
 // fp32 Q8.8 values are in the shared stage buffer at st_end - 2W; writes its
 // partial-sum words to xs (S-local).  ty: S-local heap types; fm: the
 // S-sub-tree's frozen-mask words.  One warp.
+#ifndef SE_ROOT_INLINE
+#define SE_ROOT_INLINE 0
+#endif
+#if SE_ROOT_INLINE
+#define SE_ROOT_ATTR __forceinline__
+#else
+#define SE_ROOT_ATTR __noinline__
+#endif
 template <bool SP>
-__device__ __noinline__ void root(float *st_end, uint32_t *xs, const uint8_t *ty, const uint32_t *fm, uint32_t S,
+__device__ SE_ROOT_ATTR void root(float *st_end, uint32_t *xs, const uint8_t *ty, const uint32_t *fm, uint32_t S,
                                   int dS, int d0, uint32_t j0)
 {
     const int lane = threadIdx.x & 31;
