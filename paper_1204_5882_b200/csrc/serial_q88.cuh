@@ -50,6 +50,7 @@
 #endif
 
 
+
 namespace se {
 
 #ifdef SE_PROF
@@ -348,8 +349,10 @@ __device__ __noinline__ uint32_t w32(int v, uint32_t m32)
     // SASS instructions, none of them BSSY).  c2..c5 +4.6 .. +7.3 %.  The same
     // trick on the width-8 fallback, the wide levels' types, the register
     // walk's type masks or per node costs 3-5 % (profiles/r02/ab_uniform.txt):
-    // there the uniform value turns selects into branches or sits on the
-    // address path.
+    // ptxas keeps a value uniform only while uniform registers are free along the
+    // call chain: with the walk's type masks in uniform registers (live across
+    // the w32 calls) this function falls back to the divergent form (806
+    // instructions) and nothing is gained in the walk itself.
     m32 = __reduce_or_sync(0xffffffffu, m32);
 #endif
     const uint32_t r = w32_body(v, m32);
@@ -812,8 +815,10 @@ __device__ __forceinline__ void wide(float *st_end, uint32_t *xs, const uint8_t 
 // partial-sum words to xs (S-local).  ty: S-local heap types; fm: the
 // S-sub-tree's frozen-mask words.  One warp.
 #ifndef SE_ROOT_INLINE
-#define SE_ROOT_INLINE 0
+#define SE_ROOT_INLINE 1
 #endif
+// inlined into sc_decode_kernel (its only caller): c3 +5 %, c4 +6.6 %, c5 +1.8 %
+// against the out-of-line call (profiles/r02/ab_uniform.txt)
 #if SE_ROOT_INLINE
 #define SE_ROOT_ATTR __forceinline__
 #else
