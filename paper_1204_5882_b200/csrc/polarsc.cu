@@ -1913,7 +1913,7 @@ __global__ void __launch_bounds__(NT, NT == 512 ? 1 : 2) sc_decode_kernel(DecPar
 #define PQ_WALK2 1
 #endif
                         if (se2)
-                            se::root<CL && (SE_W32_NPAT > 0)>(sm.st + 2 * S, sm.xs, sm.ty, sm.fm, S, dS, d, j);
+                            se::root<(CL || SE_SP_ALL) && (SE_W32_NPAT > 0)>(sm.st + 2 * S, sm.xs, sm.ty, sm.fm, S, dS, d, j);
                         else if (!p.plain && fc.dump == nullptr && W > 512)
                             warp_wide_root<FM>(sm.st + 2 * S, sm.xs, sm.ty, S, dS, d, j);
                         else if (PQ_WALK2 && !p.plain && fc.dump == nullptr && W >= 64)

@@ -478,6 +478,10 @@ __device__ __noinline__ uint32_t w32s(int v)
 #ifndef SE_W32_NPAT
 #define SE_W32_NPAT 2
 #endif
+#ifndef SE_SP_ALL
+#define SE_SP_ALL 0  // 1: the pattern routines in the unclustered kernels too (measured slower)
+#endif
+#define SE_W32_P0(X)
 #define SE_W32_P1(X) X(0x1u)
 #define SE_W32_P2(X) SE_W32_P1(X) X(0x10117u)
 #define SE_W32_P4(X) SE_W32_P2(X) X(0x177f7fffu) X(0x117177fu)
