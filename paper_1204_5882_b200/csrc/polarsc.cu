@@ -933,14 +933,61 @@ __device__ __forceinline__ void combine_block(uint32_t *x, uint32_t lpos, uint32
 // cluster-sliced word ranges of the global partial sums (W >= S >= 2048 bits,
 // so every CTA of a cluster of <= 8 gets >= 8 words): words [b, b + nw) = 0,
 // and words [b, b + nw) ^= words [b + nw, b + 2 nw)
+// (16-byte accesses, four independent load pairs in flight per thread: one
+// thread's words are dependent L2 round trips otherwise -- the combine steps
+// were 10 % of the upper band's samples with the scalar loop)
+// Out of line (PQ_COMBINE_OOL): inlined, the batched loads raise the kernel's
+// register pressure and ptxas spills in the serial band (every config -10 %).
+#ifndef PQ_COMBINE_V4
+#define PQ_COMBINE_V4 1
+#endif
+#ifndef PQ_COMBINE_OOL
+#define PQ_COMBINE_OOL 0
+#endif
+#ifndef PQ_COMBINE_U
+#define PQ_COMBINE_U 1  // uint4 load pairs in flight per thread (2 or more: the serial band's compile degrades)
+#endif
+#if PQ_COMBINE_OOL
+#define PQ_COMBINE_ATTR __noinline__
+#else
+#define PQ_COMBINE_ATTR __forceinline__
+#endif
 __device__ __forceinline__ void zero_words_slice(uint32_t *x, uint32_t b, uint32_t nw, uint32_t rank, uint32_t K)
 {
     const uint32_t q = nw / K, w0 = rank * q;
+    if (PQ_COMBINE_V4 && q % 4 == 0 && (reinterpret_cast<uintptr_t>(x + b + w0) & 15u) == 0) {  // else: the word loop
+        uint4 *xa = reinterpret_cast<uint4 *>(x + b + w0);
+        for (uint32_t i = threadIdx.x; i < q / 4; i += blockDim.x) xa[i] = make_uint4(0u, 0u, 0u, 0u);
+        return;
+    }
     for (uint32_t w = w0 + threadIdx.x; w < w0 + q; w += blockDim.x) x[b + w] = 0;
 }
-__device__ __forceinline__ void combine_words_slice(uint32_t *x, uint32_t b, uint32_t nw, uint32_t rank, uint32_t K)
+__device__ PQ_COMBINE_ATTR void combine_words_slice(uint32_t *x, uint32_t b, uint32_t nw, uint32_t rank, uint32_t K)
 {
     const uint32_t q = nw / K, w0 = rank * q;
+    if (PQ_COMBINE_V4 && q % 4 == 0 && (reinterpret_cast<uintptr_t>(x + b + w0) & 15u) == 0) {
+        uint4 *xa = reinterpret_cast<uint4 *>(x + b + w0);
+        const uint4 *xb = reinterpret_cast<const uint4 *>(x + b + nw + w0);
+        const uint32_t q4 = q / 4, nthr = blockDim.x;
+#pragma unroll 1
+        for (uint32_t i0 = threadIdx.x; i0 < q4; i0 += PQ_COMBINE_U * nthr) {
+            uint4 l[PQ_COMBINE_U], r[PQ_COMBINE_U];
+#pragma unroll
+            for (int k = 0; k < PQ_COMBINE_U; k++) {
+                const uint32_t i = i0 + k * nthr;
+                if (i < q4) {
+                    l[k] = xa[i];
+                    r[k] = xb[i];
+                }
+            }
+#pragma unroll
+            for (int k = 0; k < PQ_COMBINE_U; k++) {
+                const uint32_t i = i0 + k * nthr;
+                if (i < q4) xa[i] = make_uint4(l[k].x ^ r[k].x, l[k].y ^ r[k].y, l[k].z ^ r[k].z, l[k].w ^ r[k].w);
+            }
+        }
+        return;
+    }
     for (uint32_t w = w0 + threadIdx.x; w < w0 + q; w += blockDim.x) x[b + w] ^= x[b + nw + w];
 }
 
@@ -1509,6 +1556,7 @@ struct UpSrc {
 
 struct Ring {
     uint64_t *bar;   // D mbarriers
+    uint32_t *cnt;   // D counters: warps that have left the stage (PQ_RING_WARPREL)
     float *base;     // ring start in shared memory
     uint32_t C;      // elements per chunk (multiple of 256)
     uint32_t D;      // stages
@@ -1528,42 +1576,65 @@ struct Ring {
 // ef: the stage operands are read for the last time (a g-step reads its
 // parent node once, after the left sub-tree), so they are loaded evict-first
 // and leave L2 to the children the next steps re-read
-__device__ __forceinline__ void ring_issue(const Ring &r, const UpSrc &u, uint32_t e0, uint32_t s, bool ef = false)
+__device__ __forceinline__ uint32_t ring_bytes(const UpSrc &u, uint32_t C)
 {
-    unsigned char *st = reinterpret_cast<unsigned char *>(r.base) + (size_t)s * r.sbytes;
-    const uint32_t C = r.C, wb = C / 8;  // bytes of C bits
+    const uint32_t wb = C / 8;  // bytes of C bits
     uint32_t bytes = 0;
     if (u.a) bytes += 8 * C;
     if (u.a16) bytes += 4 * C;
     if (u.ya) bytes += 2 * wb;
     if (u.ca) bytes += 2 * wb;
     if (u.xl) bytes += wb;
-    mbar_expect_tx(&r.bar[s], bytes);
+    return bytes;
+}
+
+// the bulk copies of one C-element chunk (operand offset e0) into the stage at st
+__device__ __forceinline__ void ring_copies(const UpSrc &u, unsigned char *st, uint32_t C, uint32_t e0, uint64_t *bar,
+                                            bool ef)
+{
+    const uint32_t wb = C / 8;
     if (u.a && ef) {
-        bulk_g2s_ef(st, u.a + e0, 4 * C, &r.bar[s]);
-        bulk_g2s_ef(st + 4 * C, u.b + e0, 4 * C, &r.bar[s]);
+        bulk_g2s_ef(st, u.a + e0, 4 * C, bar);
+        bulk_g2s_ef(st + 4 * C, u.b + e0, 4 * C, bar);
     } else if (u.a) {
-        bulk_g2s(st, u.a + e0, 4 * C, &r.bar[s]);
-        bulk_g2s(st + 4 * C, u.b + e0, 4 * C, &r.bar[s]);
+        bulk_g2s(st, u.a + e0, 4 * C, bar);
+        bulk_g2s(st + 4 * C, u.b + e0, 4 * C, bar);
     }
     if (u.a16) {
-        bulk_g2s(st, u.a16 + e0, 2 * C, &r.bar[s]);
-        bulk_g2s(st + 4 * C, u.b16 + e0, 2 * C, &r.bar[s]);
+        bulk_g2s(st, u.a16 + e0, 2 * C, bar);
+        bulk_g2s(st + 4 * C, u.b16 + e0, 2 * C, bar);
     }
     if (u.ya) {
-        bulk_g2s(st + 8 * C, u.ya + e0 / 32, wb, &r.bar[s]);
-        bulk_g2s(st + 8 * C + wb, u.yb + e0 / 32, wb, &r.bar[s]);
+        bulk_g2s(st + 8 * C, u.ya + e0 / 32, wb, bar);
+        bulk_g2s(st + 8 * C + wb, u.yb + e0 / 32, wb, bar);
     }
     if (u.ca) {
-        bulk_g2s(st + 8 * C + 2 * wb, u.ca + e0 / 32, wb, &r.bar[s]);
-        bulk_g2s(st + 8 * C + 3 * wb, u.cb + e0 / 32, wb, &r.bar[s]);
+        bulk_g2s(st + 8 * C + 2 * wb, u.ca + e0 / 32, wb, bar);
+        bulk_g2s(st + 8 * C + 3 * wb, u.cb + e0 / 32, wb, bar);
     }
-    if (u.xl) bulk_g2s(st + 8 * C + 4 * wb, u.xl + e0 / 32, wb, &r.bar[s]);
+    if (u.xl) bulk_g2s(st + 8 * C + 4 * wb, u.xl + e0 / 32, wb, bar);
 }
+
+__device__ __forceinline__ void ring_issue(const Ring &r, const UpSrc &u, uint32_t e0, uint32_t s, bool ef = false)
+{
+    unsigned char *st = reinterpret_cast<unsigned char *>(r.base) + (size_t)s * r.sbytes;
+    mbar_expect_tx(&r.bar[s], ring_bytes(u, r.C));
+    ring_copies(u, st, r.C, e0, &r.bar[s], ef);
+}
+
+// what the ring steps need of DecParams (passed by value: the steps can be
+// compiled out of line, PQ_RING_OOL)
+struct ChanQ {
+    float mag;
+    int fixed;
+};
+#ifndef PQ_RING_OOL
+#define PQ_RING_OOL 3
+#endif
 
 // four consecutive operands (k % 4 == 0) of one half from a landed stage
 template <int FM>
-__device__ __forceinline__ float4 ring_val4(const DecParams &p, const UpSrc &u, const unsigned char *st,
+__device__ __forceinline__ float4 ring_val4(const ChanQ &p, const UpSrc &u, const unsigned char *st,
                                             uint32_t C, int half, uint32_t k)
 {
     const uint32_t wb = C / 8;
@@ -1600,6 +1671,36 @@ __device__ __forceinline__ float4 ring_val4(const DecParams &p, const UpSrc &u, 
     return v;
 }
 
+// A warp is done with stage s.  PQ_RING_WARPREL = 0: a CTA barrier per chunk,
+// thread 0 refills the stage.  1: no barrier -- every warp counts itself out
+// of the stage (its reads ordered before the count) and the last one out
+// refills it, so warps run ahead of each other by up to D - 1 chunks instead
+// of all waiting for the slowest one at every chunk.
+// PQ_RING_WARPREL / PQ_FUSE2: 0 = off, 1 = every kernel, 2 = the clustered kernels only
+#ifndef PQ_RING_WARPREL
+#define PQ_RING_WARPREL 0
+#endif
+#define PQ_MODE_ON(mode, CL) ((mode) == 1 || ((mode) == 2 && (CL)))
+template <bool WR, class Issue>
+__device__ __forceinline__ void ring_release(const Ring &r, uint32_t s, bool more, Issue issue)
+{
+    if constexpr (WR) {
+        __syncwarp();
+        if ((threadIdx.x & 31) == 0) {
+            __threadfence_block();
+            const uint32_t old = atomicAdd(&r.cnt[s], 1u);
+            if (old + 1 == (blockDim.x >> 5)) {
+                r.cnt[s] = 0;
+                __threadfence_block();
+                if (more) issue();
+            }
+        }
+    } else {
+        __syncthreads();  // stage s fully consumed
+        if (threadIdx.x == 0 && more) issue();
+    }
+}
+
 // One upper step over output elements [lo, hi) of this CTA through the ring:
 // f-step (IS_G = false) or g-step with the left child's partial sums.
 // dst: the output stage vector (global, or shared memory for a width-S
@@ -1607,9 +1708,9 @@ __device__ __forceinline__ float4 ring_val4(const DecParams &p, const UpSrc &u, 
 // CTA-uniform parity bit of every stage's mbarrier.
 // SCR = true: both operands are fp32 stage vectors (no channel input, coset
 // or received-bit words) -- the common case, compiled without those branches
-template <int FM, bool IS_G, bool SCR>
-__device__ __forceinline__ void ring_step(const DecParams &p, const Ring &r, const UpSrc &u, float *dst, uint32_t lo,
-                                          uint32_t hi, uint32_t &ph, bool ef_f = false)
+template <int FM, bool IS_G, bool SCR, bool WR>
+__device__ __forceinline__ uint32_t ring_step_impl(const ChanQ p, const Ring r, const UpSrc u, float *dst, uint32_t lo,
+                                                  uint32_t hi, uint32_t ph, bool ef_f)
 {
     const uint32_t C = r.C, D = r.D, tid = threadIdx.x, nthr = blockDim.x;
     const bool ef = IS_G ? (bool)PQ_G_EVICT_FIRST : ef_f;
@@ -1655,10 +1756,126 @@ __device__ __forceinline__ void ring_step(const DecParams &p, const Ring &r, con
             *reinterpret_cast<float4 *>(dst + e0 + k) = v;
 #endif
         }
-        __syncthreads();  // stage s fully consumed
-        if (tid == 0 && c + D < nch) ring_issue(r, u, lo + (c + D) * C, s, ef);
+        ring_release<WR>(r, s, c + D < nch, [&]() { ring_issue(r, u, lo + (c + D) * C, s, ef); });
         s = s + 1 == D ? 0 : s + 1;
     }
+    return ph;
+}
+
+// Two upper steps in one pass (PQ_FUSE2): the step into a child of width 2*Hh
+// (f-step, or g-step with the left sibling's partial sums) fused with the
+// f-step into that child's left child.  Every child of the upper band is
+// consumed by an f-step right after it is written; here the thread that
+// computes child elements i and i + Hh (from four operand quads instead of
+// two) also computes the grandchild element f(c[i], c[i + Hh]) from its
+// registers, so the child is written once (the later g-step reads it) but
+// never re-read by an f-step: a third of the level's stage bytes, one ring
+// pass and its barriers less.  A stage holds two half-size sub-stages in the
+// ordinary layout (chunk offsets e0 and e0 + Hh); [lo, hi) is this CTA's
+// slice of the grandchild's index range.
+#ifndef PQ_FUSE2
+#define PQ_FUSE2 0
+#endif
+template <int FM, bool IS_G, bool SCR, bool WR>
+__device__ __forceinline__ uint32_t ring_step2_impl(const ChanQ p, const Ring r, const UpSrc u, float *dst1, float *dst2,
+                                                   uint32_t Hh, uint32_t lo, uint32_t hi, uint32_t ph)
+{
+    const uint32_t C2 = r.C / 2, D = r.D, tid = threadIdx.x, nthr = blockDim.x;
+    const uint32_t sb2 = r.sbytes / 2;  // 8 C2 + 5 (C2 / 8)
+    const bool ef = IS_G ? (bool)PQ_G_EVICT_FIRST : false;
+    const uint32_t nch = (hi - lo) / C2;
+    const uint32_t tx = 2 * ring_bytes(u, C2);
+    auto issue = [&](uint32_t c, uint32_t s) {
+        unsigned char *st = reinterpret_cast<unsigned char *>(r.base) + (size_t)s * r.sbytes;
+        mbar_expect_tx(&r.bar[s], tx);
+        ring_copies(u, st, C2, lo + c * C2, &r.bar[s], ef);
+        ring_copies(u, st + sb2, C2, Hh + lo + c * C2, &r.bar[s], ef);
+    };
+    if (tid == 0)
+        for (uint32_t c = 0; c < nch && c < D; c++) issue(c, c);
+    uint32_t s = 0;
+    for (uint32_t c = 0; c < nch; c++) {
+        PQ_JITTER();
+        mbar_wait(&r.bar[s], (ph >> s) & 1u);
+        ph ^= 1u << s;
+        const unsigned char *st0 = reinterpret_cast<const unsigned char *>(r.base) + (size_t)s * r.sbytes;
+        const unsigned char *st1 = st0 + sb2;
+        const uint32_t e0 = lo + c * C2;
+#pragma unroll 1
+        for (uint32_t k = 4 * tid; k < C2; k += 4 * nthr) {
+            const float4 a0 = SCR ? *reinterpret_cast<const float4 *>(st0 + 4 * k) : ring_val4<FM>(p, u, st0, C2, 0, k);
+            const float4 b0 =
+                SCR ? *reinterpret_cast<const float4 *>(st0 + 4 * (size_t)C2 + 4 * k) : ring_val4<FM>(p, u, st0, C2, 1, k);
+            const float4 a1 = SCR ? *reinterpret_cast<const float4 *>(st1 + 4 * k) : ring_val4<FM>(p, u, st1, C2, 0, k);
+            const float4 b1 =
+                SCR ? *reinterpret_cast<const float4 *>(st1 + 4 * (size_t)C2 + 4 * k) : ring_val4<FM>(p, u, st1, C2, 1, k);
+            float4 c0, c1, v;
+            if (IS_G) {
+                const uint32_t *xw0 = reinterpret_cast<const uint32_t *>(st0 + 8 * C2 + 4 * (C2 / 8));
+                const uint32_t *xw1 = reinterpret_cast<const uint32_t *>(st1 + 8 * C2 + 4 * (C2 / 8));
+                const uint32_t s0 = (xw0[k >> 5] >> (k & 31)) & 15u, s1 = (xw1[k >> 5] >> (k & 31)) & 15u;
+                c0.x = pq_gt<FM>(a0.x, b0.x, s0 & 1u);
+                c0.y = pq_gt<FM>(a0.y, b0.y, s0 & 2u);
+                c0.z = pq_gt<FM>(a0.z, b0.z, s0 & 4u);
+                c0.w = pq_gt<FM>(a0.w, b0.w, s0 & 8u);
+                c1.x = pq_gt<FM>(a1.x, b1.x, s1 & 1u);
+                c1.y = pq_gt<FM>(a1.y, b1.y, s1 & 2u);
+                c1.z = pq_gt<FM>(a1.z, b1.z, s1 & 4u);
+                c1.w = pq_gt<FM>(a1.w, b1.w, s1 & 8u);
+            } else {
+                c0.x = pq_f<FM>(a0.x, b0.x);
+                c0.y = pq_f<FM>(a0.y, b0.y);
+                c0.z = pq_f<FM>(a0.z, b0.z);
+                c0.w = pq_f<FM>(a0.w, b0.w);
+                c1.x = pq_f<FM>(a1.x, b1.x);
+                c1.y = pq_f<FM>(a1.y, b1.y);
+                c1.z = pq_f<FM>(a1.z, b1.z);
+                c1.w = pq_f<FM>(a1.w, b1.w);
+            }
+            *reinterpret_cast<float4 *>(dst1 + e0 + k) = c0;
+            *reinterpret_cast<float4 *>(dst1 + Hh + e0 + k) = c1;
+            v.x = pq_f<FM>(c0.x, c1.x);
+            v.y = pq_f<FM>(c0.y, c1.y);
+            v.z = pq_f<FM>(c0.z, c1.z);
+            v.w = pq_f<FM>(c0.w, c1.w);
+            *reinterpret_cast<float4 *>(dst2 + e0 + k) = v;
+        }
+        ring_release<WR>(r, s, c + D < nch, [&]() { issue(c + D, s); });
+        s = s + 1 == D ? 0 : s + 1;
+    }
+    return ph;
+}
+
+// The ring steps out of line (OOL) or inlined into the walk.  Out of line the
+// kernel body is ~2000 instructions shorter and the serial engine inlined into
+// it compiles a little better: c3 / c4 +1.5 %; the clustered kernels lose
+// 1.2 % (c5), so PQ_RING_OOL = 3 takes it for the unclustered kernels only
+// (0: never, 1: always).
+template <int FM, bool IS_G, bool SCR, bool WR>
+__device__ __noinline__ uint32_t ring_step_ool(const ChanQ p, const Ring r, const UpSrc u, float *dst, uint32_t lo,
+                                               uint32_t hi, uint32_t ph, bool ef_f)
+{
+    return ring_step_impl<FM, IS_G, SCR, WR>(p, r, u, dst, lo, hi, ph, ef_f);
+}
+template <int FM, bool IS_G, bool SCR, bool WR, bool OOL>
+__device__ __forceinline__ uint32_t ring_step(const ChanQ p, const Ring r, const UpSrc u, float *dst, uint32_t lo,
+                                              uint32_t hi, uint32_t ph, bool ef_f = false)
+{
+    if constexpr (OOL) return ring_step_ool<FM, IS_G, SCR, WR>(p, r, u, dst, lo, hi, ph, ef_f);
+    else return ring_step_impl<FM, IS_G, SCR, WR>(p, r, u, dst, lo, hi, ph, ef_f);
+}
+template <int FM, bool IS_G, bool SCR, bool WR>
+__device__ __noinline__ uint32_t ring_step2_ool(const ChanQ p, const Ring r, const UpSrc u, float *dst1, float *dst2,
+                                                uint32_t Hh, uint32_t lo, uint32_t hi, uint32_t ph)
+{
+    return ring_step2_impl<FM, IS_G, SCR, WR>(p, r, u, dst1, dst2, Hh, lo, hi, ph);
+}
+template <int FM, bool IS_G, bool SCR, bool WR, bool OOL>
+__device__ __forceinline__ uint32_t ring_step2(const ChanQ p, const Ring r, const UpSrc u, float *dst1, float *dst2,
+                                               uint32_t Hh, uint32_t lo, uint32_t hi, uint32_t ph)
+{
+    if constexpr (OOL) return ring_step2_ool<FM, IS_G, SCR, WR>(p, r, u, dst1, dst2, Hh, lo, hi, ph);
+    else return ring_step2_impl<FM, IS_G, SCR, WR>(p, r, u, dst1, dst2, Hh, lo, hi, ph);
 }
 
 // ---- thread-block clusters: K CTAs share one frame's upper band
@@ -1702,6 +1919,8 @@ __global__ void __launch_bounds__(NT, NT == 512 ? 1 : 2) sc_decode_kernel(DecPar
         p.dump = nullptr;
         p.prof = nullptr;
     }
+    constexpr bool WR = PQ_MODE_ON(PQ_RING_WARPREL, CL), FUSE2 = PQ_MODE_ON(PQ_FUSE2, CL);
+    constexpr bool ROOL = PQ_RING_OOL == 1 || (PQ_RING_OOL == 3 && !CL);
     extern __shared__ __align__(16) unsigned char smem_raw[];
     __shared__ float red[32];
     const uint32_t S = p.S, N = p.N;
@@ -1763,24 +1982,32 @@ __global__ void __launch_bounds__(NT, NT == 512 ? 1 : 2) sc_decode_kernel(DecPar
     // TMA ring for the upper band (S >= 2048 so that chunks are >= 256 elements;
     // the stage dump keeps the register path)
     __shared__ __align__(8) uint64_t ring_bar[8];
+    __shared__ uint32_t ring_cnt[8];
     const bool use_ring = S >= 2048 && p.dump == nullptr;
     uint32_t ring_ph = 0;
     if (use_ring) {
         if (tid == 0) {
-            for (int q = 0; q < 8; q++) mbar_init(&ring_bar[q], 1);
+            for (int q = 0; q < 8; q++) {
+                mbar_init(&ring_bar[q], 1);
+                ring_cnt[q] = 0;
+            }
             asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         }
         __syncthreads();
     }
-    // two stages of S/4-element chunks over the stage area (A/B-measured on
+    // PQ_RING_DEPTH stages of S/4-element chunks over the stage area (A/B-measured on
     // c3: chunk size matters -- S/8 was 8 % slower -- depth 2 vs 3 does not:
     // with every frame streaming, the upper band then runs near HBM peak)
     Ring ring;
     ring.bar = ring_bar;
+    ring.cnt = ring_cnt;
     ring.C = S / 4;
     ring.sbytes = 8 * ring.C + 5 * (ring.C / 8);
-    ring.D = 2;
+    ring.D = WR ? 3 : 2;
     ring.base = sm.st;
+    ChanQ cq;
+    cq.mag = p.mag;
+    cq.fixed = p.fixed;
 
     __shared__ unsigned long long eng_prof[4];
     if (tid < 4) eng_prof[tid] = 0;
@@ -1819,6 +2046,14 @@ __global__ void __launch_bounds__(NT, NT == 512 ? 1 : 2) sc_decode_kernel(DecPar
     };
     // this CTA's slice [lo, hi) of a range of L elements (L / K a multiple of 32)
     auto slice_lo = [&](uint32_t L) -> uint32_t { return rank * (L / K); };
+    // may the step into the width-Wc child (dc, jc) of type tc be fused with the
+    // f-step into its left child?  Both outputs stay in the global stage buffers,
+    // the child is neither skipped (rate-0) nor guarded first (rate-1), its
+    // left child is not rate-0, and a half chunk still feeds every thread.
+    auto fuse2_ok = [&](uint32_t Wc, uint8_t tc, int dc, uint32_t jc) -> bool {
+        return !p.plain && Wc / 2 > S && ring.C / 2 >= 4u * (uint32_t)nthr && tc != NT_RATE0 && tc != NT_RATE1 &&
+               ntype(dc + 1, 2 * jc) != NT_RATE0;
+    };
 
     int d = 0;
     uint32_t j = 0;
@@ -2025,8 +2260,21 @@ __global__ void __launch_bounds__(NT, NT == 512 ? 1 : 2) sc_decode_kernel(DecPar
                 // sub-tree: when the level's parents outgrow L2 it cannot
                 // hit, so the f-step reads them evict-first as well
                 const bool f_ef = PQ_F_EF_BYTES > 0 && (uint64_t)8 * H * (gridDim.x / K) > (uint64_t)PQ_F_EF_BYTES;
-                if (ch0) ring_step<FM, false, false>(p, ring, u, dst, flo, fhi, ring_ph, f_ef);
-                else ring_step<FM, false, true>(p, ring, u, dst, flo, fhi, ring_ph, f_ef);
+                // the child is consumed by an f-step right away: both steps in one pass
+                if constexpr (FUSE2) {
+                    if (fuse2_ok(H, tl, d + 1, 2 * j)) {
+                        const uint32_t Hh = H / 2;
+                        const uint32_t lo2 = fsplit ? slice_lo(Hh) : 0, hi2 = fsplit ? lo2 + Hh / K : Hh;
+                        float *dst2 = stage_ptr(p, fc, sm, Hh);
+                        if (ch0) ring_ph = ring_step2<FM, false, false, WR, ROOL>(cq, ring, u, dst, dst2, Hh, lo2, hi2, ring_ph);
+                        else ring_ph = ring_step2<FM, false, true, WR, ROOL>(cq, ring, u, dst, dst2, Hh, lo2, hi2, ring_ph);
+                        d += 2;
+                        j = 4 * j;
+                        continue;
+                    }
+                }
+                if (ch0) ring_ph = ring_step<FM, false, false, WR, ROOL>(cq, ring, u, dst, flo, fhi, ring_ph, f_ef);
+                else ring_ph = ring_step<FM, false, true, WR, ROOL>(cq, ring, u, dst, flo, fhi, ring_ph, f_ef);
             } else if (!ch0 && W > S && (fhi - flo) % (8 * nthr) == 0) {
                 // from HBM/L2: two chunks per thread in flight
 #pragma unroll 1
@@ -2157,8 +2405,21 @@ __global__ void __launch_bounds__(NT, NT == 512 ? 1 : 2) sc_decode_kernel(DecPar
                     u.b = src + W;
                 }
                 u.xl = fc.X + (j * W) / 32;  // the left child's bits (a width-S child's were copied out)
-                if (ch0) ring_step<FM, true, false>(p, ring, u, dst, glo, ghi, ring_ph);
-                else ring_step<FM, true, true>(p, ring, u, dst, glo, ghi, ring_ph);
+                if constexpr (FUSE2) {
+                    if (fuse2_ok(W, tr, d, jr)) {
+                        const uint32_t Hh = W / 2;
+                        const uint32_t lo2 = gsplit ? slice_lo(Hh) : 0, hi2 = gsplit ? lo2 + Hh / K : Hh;
+                        float *dst2 = stage_ptr(p, fc, sm, Hh);
+                        if (ch0) ring_ph = ring_step2<FM, true, false, WR, ROOL>(cq, ring, u, dst, dst2, Hh, lo2, hi2, ring_ph);
+                        else ring_ph = ring_step2<FM, true, true, WR, ROOL>(cq, ring, u, dst, dst2, Hh, lo2, hi2, ring_ph);
+                        d += 1;
+                        j = 2 * jr;
+                        entering = true;
+                        continue;
+                    }
+                }
+                if (ch0) ring_ph = ring_step<FM, true, false, WR, ROOL>(cq, ring, u, dst, glo, ghi, ring_ph);
+                else ring_ph = ring_step<FM, true, true, WR, ROOL>(cq, ring, u, dst, glo, ghi, ring_ph);
             }
             // g-step: W >= 256 here; 4 elements per thread, 4 chunks in flight
             // (the operand loads are unswitched on the channel case)

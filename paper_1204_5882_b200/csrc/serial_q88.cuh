@@ -48,6 +48,9 @@
 #ifndef SE_UNIFORM_MASK
 #define SE_UNIFORM_MASK 1
 #endif
+#ifndef SE_DIVZ
+#define SE_DIVZ 0
+#endif
 
 
 
@@ -266,26 +269,34 @@ __device__ __forceinline__ uint32_t d8(const int (&x)[8], uint32_t m)
 
 // the width-8 child of a lane-parallel width-16 node: gather its 8 values
 // (lanes 0..7) into every lane, then the replicated pattern routines
-__device__ __forceinline__ uint32_t child8(int c, uint32_t m8, bool plain)
+//
+// z is a lane-dependent zero (SE_DIVZ): a shuffle from a constant lane is
+// warp-uniform to ptxas, which then MAY move the whole replicated width-8
+// computation to the uniform datapath (USEL / UIADD3 chains fed by R2UR
+// transfers).  Whether it does depends on the uniform registers the rest of
+// the kernel leaves free -- an unrelated edit of the upper band flipped w32
+// from 557 to 655 instructions and cost every config 12 % -- so the source
+// lane is made opaque and the replicated arithmetic stays on the vector ALUs.
+__device__ __forceinline__ uint32_t child8(int c, uint32_t m8, bool plain, int z)
 {
     SE_T0();
     int x[8];
 #pragma unroll
-    for (int i = 0; i < 8; i++) x[i] = __shfl_sync(0xffffffffu, c, i);
+    for (int i = 0; i < 8; i++) x[i] = __shfl_sync(0xffffffffu, c, i | z);
     const uint32_t r = plain ? w8plain(x[0], x[1], x[2], x[3], x[4], x[5], x[6], x[7], m8) : d8(x, m8);
     SE_T1(0);
     return r;
 }
 
-__device__ __forceinline__ uint32_t w16_body(int v, uint32_t m16);
-__device__ __forceinline__ uint32_t w16(int v, uint32_t m16)
+__device__ __forceinline__ uint32_t w16_body(int v, uint32_t m16, int z);
+__device__ __forceinline__ uint32_t w16(int v, uint32_t m16, int z)
 {
     SE_T0();
-    const uint32_t r = w16_body(v, m16);
+    const uint32_t r = w16_body(v, m16, z);
     SE_T1(1);
     return r;
 }
-__device__ __forceinline__ uint32_t w16_body(int v, uint32_t m16)
+__device__ __forceinline__ uint32_t w16_body(int v, uint32_t m16, int z)
 {
     const unsigned FULL = 0xffffffffu;
     const int lane = threadIdx.x & 31;
@@ -327,7 +338,7 @@ __device__ __forceinline__ uint32_t w16_body(int v, uint32_t m16)
             int c;
             if (side) c = gq(v, b, (xl >> lane) & 1u);
             else c = fq(v, b);
-            bits = child8(c, m8, plain);
+            bits = child8(c, m8, plain, z);
         }
         if (side) xr = bits;
         else xl = bits;
@@ -363,6 +374,11 @@ __device__ __forceinline__ uint32_t w32_body(int v, uint32_t m32)
 {
     const unsigned FULL = 0xffffffffu;
     const int lane = threadIdx.x & 31;
+#if SE_DIVZ
+    const int z = abs(v) >> 16;  // 0: Q8.8 codes are saturated to +-32767 (see child8)
+#else
+    const int z = 0;
+#endif
     const int t = ntype(m32, 32);
     if (t == T_R0) return 0u;
     if (t == T_R1) {
@@ -402,7 +418,7 @@ __device__ __forceinline__ uint32_t w32_body(int v, uint32_t m32)
             int c;
             if (side) c = gq(v, b, (xl >> lane) & 1u);
             else c = fq(v, b);
-            bits = w16(c, m16);
+            bits = w16(c, m16, z);
         }
         if (side) xr = bits;
         else xl = bits;
@@ -450,8 +466,9 @@ __device__ __forceinline__ uint32_t lnode(int v, bool &ok)
         return tot < 0 ? lm(W) : 0u;
     } else if constexpr (W == 8) {
         int x[8];
+        const int z = SE_DIVZ ? abs(v) >> 16 : 0;  // lane-dependent zero, see child8
 #pragma unroll
-        for (int i = 0; i < 8; i++) x[i] = __shfl_sync(FULL, v, i);
+        for (int i = 0; i < 8; i++) x[i] = __shfl_sync(FULL, v, i | z);
         return rnode<8, M>(x, ok);
     } else {
         constexpr int H = W / 2;

@@ -2,6 +2,7 @@
 (tools/sanitize.sh): single-CTA 256 threads, 128-thread CTAs, clusters of 4
 CTAs with 512 threads, clusters of 2 with 256; fixed point and exact f; the
 fp32, Q8.8 and BSC inputs.  Each decode is checked against the oracle."""
+import os
 import sys
 
 import numpy as np
@@ -29,8 +30,11 @@ llr += rng.normal(0, 0.7, llr.shape).astype(np.float32)  # weak / strong mix: ra
 u = np.array([O.polar_transform_bytes(xi) for xi in x])
 uw = torch.from_numpy(pack_bits(u).view(np.int32).copy()).to(dev)
 shapes = [(1, 256, 13), (1, 128, 12), (4, 0, 11), (2, 256, 11), (1, 64, 11)]
+if os.environ.get("PQ_SHAPES"):  # "cluster,threads,log2S;..." (e.g. the fused / warp-release ring builds)
+    shapes = [tuple(int(v) for v in t.split(",")) for t in os.environ["PQ_SHAPES"].split(";")]
+modes = ("fixed",) if os.environ.get("PQ_FIXED_ONLY") else ("fixed", "exact")
 bad = 0
-for fmode in ("fixed", "exact"):
+for fmode in modes:
     prec = 16 if fmode == "fixed" else 32
     ref = O.sc_decode_batch(mask, llr, u, precision=prec, threads=8)
     for ncl, thr, lg in shapes:
