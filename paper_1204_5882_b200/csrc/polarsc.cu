@@ -312,12 +312,33 @@ __device__ __forceinline__ float pq_gt(float a, float b, uint32_t s) { return qa
 // exact small integer held in a float -> int, with full-rate ALU ops
 __device__ __forceinline__ int small_f2i(float x) { return __float_as_int(x + 12582912.0f) - 0x4B400000; }
 
+// table entry for an index held as a small exact integer in a float, x in
+// [0, 2047]: x + 1.5 * 2^21 has an ulp of 1/4, so its bit pattern is
+// 0x4A400000 + 4 x -- the byte offset into the fp32 table plus a constant.
+// One integer add of (table base - 0x4A400000) gives the shared-memory
+// address: no index conversion, no scaling (PQ_F_LEA; two instructions per
+// f fewer than the index form in the upper and block bands).
+#ifndef PQ_F_LEA
+#define PQ_F_LEA 0  // measured: c3 / c4 -0.3 %, c2 +-0 (profiles/r02/ab_upper_band.txt)
+#endif
+__device__ __forceinline__ float corr_at(float x)
+{
+#if PQ_F_LEA
+    const uint32_t k = (uint32_t)__cvta_generic_to_shared(pq_corrtab) - 0x4A400000u;
+    float v;
+    asm("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(__float_as_uint(x + 3145728.0f) + k));
+    return v;
+#else
+    return pq_corrtab[small_f2i(x)];
+#endif
+}
+
 // magnitudes ma, mb (raw codes)
 __device__ __forceinline__ float pq_fmag_fixed(float ma, float mb)
 {
-    const int is = small_f2i(fminf(ma + mb, (float)(CORR_SMEM - 1)));
-    const int id = small_f2i(fminf(fabsf(ma - mb), (float)(CORR_SMEM - 1)));
-    return fmaxf(fminf(ma, mb) + pq_corrtab[is] - pq_corrtab[id], 0.0f);
+    const float cs = corr_at(fminf(ma + mb, (float)(CORR_SMEM - 1)));
+    const float cd = corr_at(fminf(fabsf(ma - mb), (float)(CORR_SMEM - 1)));
+    return fmaxf(fminf(ma, mb) + cs - cd, 0.0f);
 }
 
 template <int FM>
@@ -1680,6 +1701,9 @@ __device__ __forceinline__ float4 ring_val4(const ChanQ &p, const UpSrc &u, cons
 #ifndef PQ_RING_WARPREL
 #define PQ_RING_WARPREL 0
 #endif
+#ifndef PQ_RING_UNROLL2
+#define PQ_RING_UNROLL2 0
+#endif
 #define PQ_MODE_ON(mode, CL) ((mode) == 1 || ((mode) == 2 && (CL)))
 template <bool WR, class Issue>
 __device__ __forceinline__ void ring_release(const Ring &r, uint32_t s, bool more, Issue issue)
@@ -1729,15 +1753,17 @@ __device__ __forceinline__ uint32_t ring_step_impl(const ChanQ p, const Ring r, 
         ph ^= 1u << s;
         const unsigned char *st = reinterpret_cast<const unsigned char *>(r.base) + (size_t)s * r.sbytes;
         const uint32_t e0 = lo + c * C;
-#pragma unroll 1
-        for (uint32_t k = 4 * tid; k < C; k += 4 * nthr) {
-            const float4 a = SCR ? *reinterpret_cast<const float4 *>(st + 4 * k) : ring_val4<FM>(p, u, st, C, 0, k);
-            const float4 b =
-                SCR ? *reinterpret_cast<const float4 *>(st + 4 * (size_t)C + 4 * k) : ring_val4<FM>(p, u, st, C, 1, k);
+        auto ld = [&](int half, uint32_t k) -> float4 {
+            return SCR ? *reinterpret_cast<const float4 *>(st + (size_t)half * 4 * C + 4 * k)
+                       : ring_val4<FM>(p, u, st, C, half, k);
+        };
+        auto sgn = [&](uint32_t k) -> uint32_t {
+            const uint32_t *xw = reinterpret_cast<const uint32_t *>(st + 8 * C + 4 * (C / 8));
+            return IS_G ? (xw[k >> 5] >> (k & 31)) & 15u : 0u;
+        };
+        auto comp = [&](const float4 &a, const float4 &b, uint32_t sb) -> float4 {
             float4 v;
             if (IS_G) {
-                const uint32_t *xw = reinterpret_cast<const uint32_t *>(st + 8 * C + 4 * (C / 8));
-                const uint32_t sb = (xw[k >> 5] >> (k & 31)) & 15u;
                 v.x = pq_gt<FM>(a.x, b.x, sb & 1u);
                 v.y = pq_gt<FM>(a.y, b.y, sb & 2u);
                 v.z = pq_gt<FM>(a.z, b.z, sb & 4u);
@@ -1748,6 +1774,9 @@ __device__ __forceinline__ uint32_t ring_step_impl(const ChanQ p, const Ring r, 
                 v.z = pq_f<FM>(a.z, b.z);
                 v.w = pq_f<FM>(a.w, b.w);
             }
+            return v;
+        };
+        auto put = [&](uint32_t k, const float4 &v) {
 #if PQ_ST_EVICT_LAST
             asm volatile("st.global.L2::cache_hint.v4.f32 [%0], {%1, %2, %3, %4}, %5;" ::"l"(dst + e0 + k), "f"(v.x),
                          "f"(v.y), "f"(v.z), "f"(v.w), "l"(st_pol)
@@ -1755,7 +1784,23 @@ __device__ __forceinline__ uint32_t ring_step_impl(const ChanQ p, const Ring r, 
 #else
             *reinterpret_cast<float4 *>(dst + e0 + k) = v;
 #endif
+        };
+        const uint32_t kstep = 4 * nthr;
+        uint32_t k = 4 * tid;
+#if PQ_RING_UNROLL2
+        // two quads per thread in flight (all loads ahead of the stores: dst is a
+        // generic pointer, so the compiler cannot move a load across a store)
+#pragma unroll 1
+        for (; k + kstep < C; k += 2 * kstep) {
+            const float4 a0 = ld(0, k), b0 = ld(1, k), a1 = ld(0, k + kstep), b1 = ld(1, k + kstep);
+            const uint32_t s0 = sgn(k), s1 = sgn(k + kstep);
+            const float4 v0 = comp(a0, b0, s0), v1 = comp(a1, b1, s1);
+            put(k, v0);
+            put(k + kstep, v1);
         }
+#endif
+#pragma unroll 1
+        for (; k < C; k += kstep) put(k, comp(ld(0, k), ld(1, k), sgn(k)));
         ring_release<WR>(r, s, c + D < nch, [&]() { ring_issue(r, u, lo + (c + D) * C, s, ef); });
         s = s + 1 == D ? 0 : s + 1;
     }
