@@ -64,5 +64,59 @@ def build(force: bool = False, verbose: bool = False) -> str:
     return OUT
 
 
+# the fixed-point production kernels: <FM=3, clustered, diag=0, threads>
+CENSUS_KERNELS = {"unclustered": "ILi3ELb0ELb0ELi256", "clustered512": "ILi3ELb1ELb0ELi512",
+                  "clustered256": "ILi3ELb1ELb0ELi256"}
+
+
+def census(lib: str = OUT) -> dict:
+    """Compiled form of the serial engine in a built library (CPU only:
+    cuobjdump + nvdisasm, ~15 s).  ptxas allocates se::w32 / se::walk together
+    with each kernel's body, and an unrelated edit can leave se::walk short of
+    registers (spill stores, -10 % on every config) or move se::w32's
+    replicated arithmetic to the uniform datapath (R2UR transfers, -4 %):
+    DESIGN.md section 7, profiles/r02/ab_upper_band.txt.  Returns, per
+    production kernel, instruction counts of the body / w32 / walk, R2UR in w32
+    and STL (spill stores) in w32 and walk."""
+    import re
+    import shutil
+    import tempfile
+    tmp = tempfile.mkdtemp(prefix="pq_census_")
+    try:
+        subprocess.run(["cuobjdump", "-xelf", "all", os.path.abspath(lib)], cwd=tmp, check=True,
+                       stdout=subprocess.DEVNULL, stderr=subprocess.DEVNULL)
+        cubins = [f for f in os.listdir(tmp) if f.startswith("polarsc") and f.endswith(".cubin")]
+        if not cubins:
+            raise RuntimeError(f"no polarsc cubin in {lib}")
+        cubin = max(cubins, key=lambda f: os.path.getsize(os.path.join(tmp, f)))
+        dis = subprocess.run(["nvdisasm", "-c", cubin], cwd=tmp, check=True, capture_output=True, text=True).stdout
+    finally:
+        shutil.rmtree(tmp, ignore_errors=True)
+    out = {k: {"body": 0, "w32": 0, "walk": 0, "w32_r2ur": 0, "w32_stl": 0, "walk_stl": 0} for k in CENSUS_KERNELS}
+    label = re.compile(r"^(\$?_Z\S*):\s*$")
+    cur, which, part = None, None, None
+    for line in dis.splitlines():
+        m = label.match(line)
+        if m:
+            cur = m.group(1)
+            which = next((k for k, tag in CENSUS_KERNELS.items() if tag in cur), None)
+            part = ("w32" if "_ZN2se3w32Eij" in cur else "walk" if "_ZN2se4walk" in cur
+                    else "body" if cur.count("$") == 0 else None)
+            continue
+        if which is None or part is None or "/*" not in line[:16]:
+            continue
+        d = out[which]
+        d[part] += 1
+        if part == "w32" and "R2UR" in line:
+            d["w32_r2ur"] += 1
+        if " STL" in line and part in ("w32", "walk"):
+            d[part + "_stl"] += 1
+    return out
+
+
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    if "--census" in sys.argv:
+        import json
+        print(json.dumps(census(), indent=1))
+    else:
+        print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
