@@ -65,8 +65,9 @@ def build(force: bool = False, verbose: bool = False) -> str:
 
 
 # the fixed-point production kernels: <FM=3, clustered, diag=0, threads>
-CENSUS_KERNELS = {"unclustered": "ILi3ELb0ELb0ELi256", "clustered512": "ILi3ELb1ELb0ELi512",
-                  "clustered256": "ILi3ELb1ELb0ELi256"}
+CENSUS_KERNELS = {"unclustered": "ILi3ELb0ELb0ELi256ELi0E", "clustered512_k2": "ILi3ELb1ELb0ELi512ELi2E",
+                  "clustered512_k4": "ILi3ELb1ELb0ELi512ELi4E", "clustered512_k8": "ILi3ELb1ELb0ELi512ELi8E",
+                  "clustered512": "ILi3ELb1ELb0ELi512ELi0E", "clustered256": "ILi3ELb1ELb0ELi256ELi0E"}
 
 
 def census(lib: str = OUT) -> dict:

@@ -31,6 +31,7 @@ def test_serial_engine_does_not_spill(cen):
         assert d["walk_stl"] == 0 and d["w32_stl"] == 0, (name, d)
 
 
-def test_unclustered_w32_is_the_vector_form(cen):
-    d = cen["unclustered"]
-    assert d["w32_r2ur"] == 0, d
+def test_bench_kernels_w32_is_the_vector_form(cen):
+    # c2-c4 run the unclustered kernel, c5 the 512-thread kernel with K = 4 compiled in
+    for name in ("unclustered", "clustered512_k2", "clustered512_k4", "clustered512_k8"):
+        assert cen[name]["w32_r2ur"] == 0, (name, cen[name])

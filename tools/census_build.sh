@@ -8,7 +8,7 @@ T=/tmp/census_$1; mkdir -p $T
 nvcc -w -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 --fmad=false -prec-div=true -ftz=false -DPQ_ONLY_FIXED $EXTRA \
      -I "$ROOT/include" -cubin -o $T/k.cubin "$ROOT/paper_1204_5882_b200/csrc/polarsc.cu"
 nvdisasm -c $T/k.cubin > $T/all.dis 2>/dev/null
-for K in ILi3ELb0ELb0ELi256 ILi3ELb1ELb0ELi512 ILi3ELb0ELb0ELi128; do
+for K in ILi3ELb0ELb0ELi256ELi0E ILi3ELb1ELb0ELi512ELi4E ILi3ELb1ELb0ELi512ELi0E; do
   awk -v K=$K '
     /^\$?_Z[^ ]*:$/ { cur=$1; next }
     /^ +\/\*[0-9a-f]+\*\// { if (index(cur,K)==0) next;

@@ -6,7 +6,7 @@
 set -e
 T=$(mktemp -d); cd $T; cuobjdump -xelf all "$OLDPWD/$1" >/dev/null 2>&1
 nvdisasm -c polarsc.sm_100a.cubin > all.dis 2>/dev/null
-for K in ILi3ELb0ELb0ELi256 ILi3ELb1ELb0ELi512 ILi3ELb0ELb0ELi128; do
+for K in ILi3ELb0ELb0ELi256ELi0E ILi3ELb1ELb0ELi512ELi4E ILi3ELb1ELb0ELi512ELi0E; do
   awk -v K=$K '/^\$?_Z[^ ]*:$/ {if (name!="") print n, name; name=$1; n=0} /^ +\/\*[0-9a-f]+\*\//{n++} END{print n,name}' all.dis \
     | grep $K | sed 's/_Z16sc_decode_kernel//; s/EEv9DecParams//g' | awk '{printf "%s=%s  ", $2, $1}'; echo
   awk -v K=$K 'BEGIN{on=0} /^\$?_Z[^ ]*:$/ {on = index($1, "_ZN2se3w32Eij")>0 && index($1,K)>0} on && /^ +\/\*[0-9a-f]+\*\//{print}' all.dis \
