@@ -701,28 +701,6 @@ __device__ __noinline__ void walk(const int *nd, uint32_t *xs, const uint8_t *ty
 // previous element's store).
 template <int W, bool FROM_F32, bool SP>
 __device__ __forceinline__ void wide(float *st_end, uint32_t *xs, const uint8_t *ty, const uint32_t *fm, uint32_t S,
-                                     int dS, int d0, uint32_t j0);
-// a wide child node (int codes): inlined, or -- SE_WIDE_OOL_MAX: widths up to
-// this one -- ONE out-of-line copy per width instead of one per call site
-// (the inlined form holds 4 copies of the width-512 routine, 2 of width 1024)
-#ifndef SE_WIDE_OOL_MAX
-#define SE_WIDE_OOL_MAX 0
-#endif
-template <int W, bool SP>
-__device__ __noinline__ void wide_ool(float *st_end, uint32_t *xs, const uint8_t *ty, const uint32_t *fm, uint32_t S,
-                                      int dS, int d0, uint32_t j0)
-{
-    wide<W, false, SP>(st_end, xs, ty, fm, S, dS, d0, j0);
-}
-template <int W, bool SP>
-__device__ __forceinline__ void wide_child(float *st_end, uint32_t *xs, const uint8_t *ty, const uint32_t *fm,
-                                           uint32_t S, int dS, int d0, uint32_t j0)
-{
-    if constexpr (W <= SE_WIDE_OOL_MAX) wide_ool<W, SP>(st_end, xs, ty, fm, S, dS, d0, j0);
-    else wide<W, false, SP>(st_end, xs, ty, fm, S, dS, d0, j0);
-}
-template <int W, bool FROM_F32, bool SP>
-__device__ __forceinline__ void wide(float *st_end, uint32_t *xs, const uint8_t *ty, const uint32_t *fm, uint32_t S,
                                      int dS, int d0, uint32_t j0)
 {
     constexpr int V = W / 32, Vh = V / 2, B = 8;
@@ -825,7 +803,7 @@ __device__ __forceinline__ void wide(float *st_end, uint32_t *xs, const uint8_t 
             for (int k = 0; k < B; k++) ch[32 * (q0 + k) + lane] = fq(a[k], b[k]);
         }
         __syncwarp();
-        if constexpr (W / 2 > SE_UNR) wide_child<W / 2, SP>(st_end, xs, ty, fm, S, dS, d0 + 1, 2 * j0);
+        if constexpr (W / 2 > SE_UNR) wide<W / 2, false, SP>(st_end, xs, ty, fm, S, dS, d0 + 1, 2 * j0);
         else walk<SP>(reinterpret_cast<const int *>(st_end - W), xs, ty, fm, S, dS, d0 + 1, 2 * j0);
     }
     if (tr == T_R0) {
@@ -846,7 +824,7 @@ __device__ __forceinline__ void wide(float *st_end, uint32_t *xs, const uint8_t 
             for (int k = 0; k < B; k++) ch[32 * (q0 + k) + lane] = gq(a[k], b[k], (sw[k] >> lane) & 1u);
         }
         __syncwarp();
-        if constexpr (W / 2 > SE_UNR) wide_child<W / 2, SP>(st_end, xs, ty, fm, S, dS, d0 + 1, 2 * j0 + 1);
+        if constexpr (W / 2 > SE_UNR) wide<W / 2, false, SP>(st_end, xs, ty, fm, S, dS, d0 + 1, 2 * j0 + 1);
         else walk<SP>(reinterpret_cast<const int *>(st_end - W), xs, ty, fm, S, dS, d0 + 1, 2 * j0 + 1);
     }
     for (int q = lane; q < Vh; q += 32) xw[q] ^= xw[Vh + q];
