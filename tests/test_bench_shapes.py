@@ -182,3 +182,24 @@ def test_fixed_serial_band_widths(cuda, warp_log2):
         dec.set_option(_lib.PQ_OPT_WARP_LOG2, warp_log2)
         uh, _ = dec.decode(torch.from_numpy(llr).to(cuda), dev_words(fz, cuda))
         assert np.array_equal(unpack_bits(uh.cpu().numpy().view(np.uint32), N), ref)
+
+
+@pytest.mark.parametrize("frames", [6, 20, 40])
+def test_cluster_size_specialised_kernels_match_oracle(cuda, frames):
+    """The 512-thread fixed-point kernels with the cluster size compiled in (K = 8, 4, 2:
+    sc_decode_kernel<.., KC>): automatic options on batches that leave SMs idle pick them;
+    every frame's u-hat equals the integer oracle's."""
+    import torch
+    if sm_count() < 80:
+        pytest.skip("shape table assumes a full B200")
+    dev = torch.device("cuda", 0)
+    code, x, u, llr = batch("c3", frames)
+    dec = ScDecoder(code, max_frames=frames, f_mode="fixed")
+    uh, _ = dec.decode(torch.from_numpy(llr).to(dev), dev_words(u, dev))
+    cfg = dec.last_config
+    want_k = 8 if frames * 8 <= sm_count() else 4 if frames * 4 <= sm_count() else 2  # choose_K
+    assert cfg["threads_per_cta"] == 512 and cfg["ctas_per_frame"] == want_k, cfg
+    got = unpack_bits(uh.cpu().numpy().view(np.uint32), code.block_size)
+    ref = oracle(code, llr, u, "fixed")
+    bad = np.flatnonzero((got != ref).any(axis=1))
+    assert bad.size == 0, f"frames {bad[:8]} differ from the oracle at shape {cfg}"
