@@ -174,8 +174,10 @@ def oracle_precision(fmode):
     """The CPU decoder beside an f mode: the Q8.8 fixed-point port for --fmode
     fixed (the paper's Table-1 technique), the fp32 mirror
     for exact (bit-exact reference of the GPU's IEEE-only f), else f64."""
-    return {"fixed": (16, "Q8.8 fixed-point SC (table boxplus)"),
-            "exact": (32, "fp32 exact SC (IEEE-only boxplus mirror)")}.get(fmode, (64, "f64 exact SC"))
+    return {"fixed": (16, "Q8.8 fixed-point SC (table boxplus), plain recursion: every node visited, "
+                          "none of the GPU path's decision-exact sub-tree shortcuts"),
+            "exact": (32, "fp32 exact SC (IEEE-only boxplus mirror), plain recursion")}.get(
+                fmode, (64, "f64 exact SC, plain recursion"))
 
 
 def cpu_baseline(code, llr, u, sample_s, threads=1, precision=16):
